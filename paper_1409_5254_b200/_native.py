@@ -1,0 +1,149 @@
+"""ctypes binding of the C ABI in include/timemg_b200.h (libtimemg_b200.so).
+
+There is no CPU fallback: if the shared library is missing or no B200 is
+visible, every solver entry point raises.  ``build()`` compiles the library
+in-tree for sm_100a (nvcc cross-compiles without a GPU).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libtimemg_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+INCLUDE = os.path.join(REPO, "include")
+MAXNT = 8
+F64, F32 = 0, 1
+E_ARG, E_UNSUPPORTED, E_NOMEM = -1, -2, -3
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
+              "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "1886"]
+
+
+class LevelDesc(ctypes.Structure):
+    _fields_ = [
+        ("n_t", ctypes.c_int32),
+        ("has_transfer", ctypes.c_int32),
+        ("n_slabs", ctypes.c_int64),
+        ("omega", ctypes.c_double),
+        ("minus_step", ctypes.c_double * (MAXNT * MAXNT)),
+        ("coupling", ctypes.c_double * (MAXNT * MAXNT)),
+        ("lu", ctypes.c_double * (MAXNT * MAXNT)),
+        ("r1", ctypes.c_double * (MAXNT * MAXNT)),
+        ("r2", ctypes.c_double * (MAXNT * MAXNT)),
+        ("perm", ctypes.c_int32 * MAXNT),
+    ]
+
+
+class PlanOpts(ctypes.Structure):
+    _fields_ = [
+        ("dtype", ctypes.c_int32),
+        ("nu1", ctypes.c_int32),
+        ("nu2", ctypes.c_int32),
+        ("gamma", ctypes.c_int32),
+        ("coarse", ctypes.c_int32),
+        ("dot_variant", ctypes.c_int32),
+        ("use_graph", ctypes.c_int32),
+        ("tail_max_slabs", ctypes.c_int32),
+    ]
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cuh")))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libtimemg_b200.so in-tree for sm_100a (skipped when up to date)."""
+    newest = max(os.path.getmtime(p) for p in sources() + [os.path.join(INCLUDE, "timemg_b200.h")])
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH + ".tmp",
+           os.path.join(CSRC, "tmg_api.cu")]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    return LIB_PATH
+
+
+_lib = None
+
+EXPORTS = ("tmg_last_error", "tmg_version", "tmg_device_check", "tmg_sweep", "tmg_residual",
+           "tmg_down", "tmg_up", "tmg_coarse_solve", "tmg_resid_norm", "tmg_plan_create",
+           "tmg_plan_destroy", "tmg_plan_cycles", "tmg_plan_solve", "tmg_plan_stats",
+           "tmg_plan_info")
+
+
+def load():
+    """Load the shared library (no GPU needed to load it)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run paper_1409_5254_b200._native.build() "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, ci, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)
+    lp = ctypes.POINTER(LevelDesc)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    L.tmg_last_error.restype = ctypes.c_char_p
+    L.tmg_version.restype = ci
+    L.tmg_device_check.argtypes = [ci]
+    L.tmg_sweep.argtypes = [ci, lp, vp, vp, vp, i64, ci, vp, vp]
+    L.tmg_residual.argtypes = [ci, lp, vp, vp, vp, i64, vp]
+    L.tmg_down.argtypes = [ci, lp, vp, vp, vp, vp, i64, ci, vp, vp]
+    L.tmg_up.argtypes = [ci, lp, vp, vp, vp, vp, vp, i64, ci, vp, vp]
+    L.tmg_coarse_solve.argtypes = [ci, lp, vp, vp, i64, ci, ci, vp]
+    L.tmg_resid_norm.argtypes = [ci, lp, vp, vp, vp, i64, vp]
+    L.tmg_plan_create.argtypes = [ctypes.POINTER(vp), lp, ci, i64, ctypes.POINTER(PlanOpts)]
+    L.tmg_plan_destroy.argtypes = [vp]
+    L.tmg_plan_cycles.argtypes = [vp, vp, vp, ci, vp]
+    L.tmg_plan_solve.argtypes = [vp, vp, vp, dp, ctypes.c_double, ci, vp]
+    L.tmg_plan_stats.argtypes = [vp, i32p, dp, i32p]
+    L.tmg_plan_info.argtypes = [vp, i32p, i32p, i32p]
+    for name in EXPORTS:
+        getattr(L, name).restype = getattr(L, name).restype or ci
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "timemg_b200"):
+    if rc == 0:
+        return
+    msg = load().tmg_last_error().decode(errors="replace")
+    if rc == E_ARG:
+        raise ValueError(f"{what}: {msg}")
+    if rc == E_UNSUPPORTED:
+        raise NotImplementedError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: CUDA error {rc}: {msg}")
+
+
+def level_desc(ops, n_slabs: int, omega: float = 1.0, r1=None, r2=None) -> LevelDesc:
+    import numpy as np
+
+    d = LevelDesc()
+    nt = int(ops.n_t)
+    d.n_t = nt
+    d.n_slabs = int(n_slabs)
+    d.omega = float(omega)
+    d.has_transfer = int(r1 is not None)
+
+    def put(field, m):
+        vals = np.ascontiguousarray(m, dtype=np.float64).ravel()
+        ctypes.memmove(ctypes.addressof(field), vals.ctypes.data, vals.nbytes)
+
+    put(d.minus_step, ops.minus_step_matrix)
+    put(d.coupling, ops.coupling)
+    put(d.lu, ops.lu.lu)
+    if r1 is not None:
+        put(d.r1, r1)
+        put(d.r2, r2)
+    for i, p in enumerate(ops.lu.perm):
+        d.perm[i] = int(p)
+    return d

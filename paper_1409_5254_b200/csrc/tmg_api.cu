@@ -1,0 +1,900 @@
+// C ABI (include/timemg_b200.h) and the cycle/iteration driver.
+//
+// The driver is the B200 counterpart of the reference's _cycle/_iterate
+// (pkg/src/timemg/multigrid.py:263-500): per cycle it enqueues
+//   down(l)   for the streaming levels l = 0 .. tl-1   (tmg_stream.cuh)
+//   tail(tl)  one CTA per problem for levels tl .. coarsest (tmg_block.cuh)
+//   up(l)     for l = tl-1 .. 0, the finest one fused with the residual
+//             norm's numpy-pairwise leaf sums
+//   finalize  exact tree sum -> sqrt -> stopping rule per problem
+// optionally captured once as a CUDA graph and replayed per cycle.  Problems
+// of a batch stop independently (per-problem active mask, like B separate
+// reference solves).  If the whole problem fits one CTA's shared memory the
+// entire solve is one launch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "timemg_b200.h"
+#include "tmg_block.cuh"
+#include "tmg_slab.cuh"
+#include "tmg_stream.cuh"
+
+using namespace tmg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess) return fail((int)e_, "%s: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKR(x)                      \
+    do {                            \
+        int r_ = (x);               \
+        if (r_ != 0) return r_;     \
+    } while (0)
+
+bool coupling_is_sparse(const tmg_level_desc &d)
+{
+    const int nt = d.n_t;
+    for (int i = 1; i < nt; ++i)
+        for (int j = 0; j < nt; ++j)
+            if (d.coupling[i * nt + j] != 0.0) return false;
+    return true;
+}
+
+template <typename T, int NT> LevelC<T, NT> make_level(const tmg_level_desc &d)
+{
+    LevelC<T, NT> L;
+    memset(&L, 0, sizeof L);
+    for (int i = 0; i < NT * NT; ++i) {
+        L.A[i] = (T)d.minus_step[i];
+        L.C[i] = (T)d.coupling[i];
+        L.lu[i] = (T)d.lu[i];
+        L.R1[i] = (T)d.r1[i];
+        L.R2[i] = (T)d.r2[i];
+    }
+    L.omega = (T)d.omega;
+    for (int i = 0; i < NT; ++i) {
+        L.perm[i] = d.perm[i];
+        unsigned m = 0;
+        for (int j = 0; j < NT; ++j) m |= (std::signbit(d.coupling[i * NT + j]) ? 1u : 0u) << j;
+        L.cneg[i] = m;
+    }
+    L.has_transfer = d.has_transfer;
+    return L;
+}
+
+int check_desc(const tmg_level_desc *d)
+{
+    if (!d) return fail(TMG_E_ARG, "level descriptor is NULL");
+    if (d->n_t < 1 || d->n_t > 4) return fail(TMG_E_UNSUPPORTED, "n_t=%d: GPU kernels support 1..4", d->n_t);
+    if (d->n_slabs < 1) return fail(TMG_E_ARG, "n_slabs must be >= 1");
+    for (int i = 0; i < d->n_t; ++i)
+        if (d->perm[i] < 0 || d->perm[i] >= d->n_t) return fail(TMG_E_ARG, "bad LU permutation");
+    return 0;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------------
+// streaming launches
+
+int sm_count()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <typename T, int NT, int NU, bool SP, bool UP>
+int launch_stream_nu(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_t s)
+{
+    auto k = stream_kernel<T, NT, NU, SP, UP>;
+    const size_t smem = RowLayout<T, NT>::smem_bytes();
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const long long warps = (long long)a.batch * a.chunks;
+    const long long grid = (warps + SW_WARPS - 1) / SW_WARPS;
+    if (grid <= 0) return 0;
+    k<<<(unsigned)grid, SW_WARPS * 32, smem, s>>>(L, a);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <typename T, int NT, bool SP, bool UP>
+int launch_stream(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, cudaStream_t s)
+{
+    switch (nu) {
+    case 0: return launch_stream_nu<T, NT, 0, SP, UP>(L, a, s);
+    case 1: return launch_stream_nu<T, NT, 1, SP, UP>(L, a, s);
+    case 2: return launch_stream_nu<T, NT, 2, SP, UP>(L, a, s);
+    case 3: return launch_stream_nu<T, NT, 3, SP, UP>(L, a, s);
+    case 4: return launch_stream_nu<T, NT, 4, SP, UP>(L, a, s);
+    default: return fail(TMG_E_UNSUPPORTED, "fused passes support nu <= 4 (got %d)", nu);
+    }
+}
+
+// rows per warp chunk: enough warps to fill the GPU several times over, a
+// multiple of the norm leaf, and long enough to amortise the warm-up row
+int chunk_rows(long long n, long long batch, int leaf_rows)
+{
+    const long long rows = (n + 31) / 32;
+    const long long target_warps = (long long)sm_count() * 16 * 4;
+    long long r = (rows * batch) / std::max(1LL, target_warps);
+    r = std::max(4LL, std::min(64LL, r));
+    const int q = std::max(1, leaf_rows);
+    r = ((r + q - 1) / q) * q;
+    return (int)std::max<long long>(r, 1);
+}
+
+template <typename T> StreamArgs<T> stream_args(long long n, long long batch, int leaf_rows)
+{
+    StreamArgs<T> a;
+    memset(&a, 0, sizeof a);
+    a.n = n;
+    a.batch = (int)batch;
+    a.rows_per_chunk = chunk_rows(n, batch, leaf_rows);
+    a.chunks = ((n + 31) / 32 + a.rows_per_chunk - 1) / a.rows_per_chunk;
+    a.leaf_rows = leaf_rows > 0 ? leaf_rows : 1;
+    return a;
+}
+
+template <typename T, int NT> bool tma_ok(const StreamArgs<T> &a, bool prolong)
+{
+    const long long rowbytes = a.n * NT * (long long)sizeof(T);
+    if (rowbytes & 15) return false;  // every problem base 16-byte aligned
+    if (!aligned16(a.f)) return false;
+    if (a.u_in && !aligned16(a.u_in)) return false;
+    if (prolong) {
+        if (((a.n / 2) * NT * (long long)sizeof(T)) & 15) return false;
+        if (!aligned16(a.uc)) return false;
+    }
+    return true;
+}
+
+// numpy pairwise leaf structure of an n-vector: n = m * 2^k with the recursion
+// splitting exactly in halves down to leaves of m <= 128 values
+int leaf_rows_for(long long n)
+{
+    long long m = n;
+    while (m > 128) {
+        if (m % 2 || (m / 2) % 8) return 0;
+        m /= 2;
+    }
+    if (m % 32) return 0;
+    return (int)(m / 32);
+}
+
+// ---------------------------------------------------------------------------
+// the plan
+
+struct PlanBase {
+    virtual ~PlanBase() {}
+    virtual int cycles(const void *f, void *u, int n_cycles, cudaStream_t s) = 0;
+    virtual int solve(const void *f, void *u, const double *floor_, double eps, int max_iters,
+                      cudaStream_t s) = 0;
+    virtual int stats(int32_t *it, double *norms, int32_t *conv) const = 0;
+    virtual int info(int32_t *kpc, int32_t *sl, int32_t *tl) const = 0;
+};
+
+}  // namespace
+
+struct tmg_plan {
+    std::unique_ptr<PlanBase> impl;
+};
+
+namespace {
+
+template <typename T, int NT, bool SP> struct Plan : PlanBase {
+    int depth = 0;
+    long long B = 0;
+    tmg_plan_opts o{};
+    std::vector<long long> n;
+    std::vector<LevelC<T, NT>> L;
+    LevelC<T, NT> *d_levels = nullptr;
+    std::vector<T *> uA, uB, fl;
+    int tl = 0;                 // first tail level
+    bool tail_smem = true;
+    size_t tail_smem_bytes = 0;
+    long long store_elems = 0;
+    T *gstore = nullptr;
+    TailArgs<T, NT> targ{};
+    // norms
+    int leaf_rows0 = 0;
+    long long nleaves = 0;
+    double *leaves = nullptr, *sqbuf = nullptr;
+    ProbState *d_st = nullptr;
+    double *d_hist = nullptr, *d_floor = nullptr;
+    int *d_active = nullptr, *d_any = nullptr, *h_any = nullptr;
+    int hist_stride = 0;
+    std::vector<int> h_it, h_conv;
+    std::vector<double> h_hist;
+    int last_max_iters = 0;
+    int kernels_per_cycle = 0;
+    // graph cache
+    cudaGraphExec_t gexec = nullptr;
+    const void *g_f = nullptr;
+    void *g_u = nullptr;
+    bool g_norm = false;
+    double g_eps = 0.0;
+    cudaStream_t ps = nullptr;  // private stream: graph capture never touches the caller's
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+
+    ~Plan() override
+    {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (ps) cudaStreamDestroy(ps);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
+        for (auto p : uA) cudaFree(p);
+        for (auto p : uB) cudaFree(p);
+        for (auto p : fl) cudaFree(p);
+        cudaFree(d_levels);
+        cudaFree(gstore);
+        cudaFree(leaves);
+        cudaFree(sqbuf);
+        cudaFree(d_st);
+        cudaFree(d_hist);
+        cudaFree(d_floor);
+        cudaFree(d_active);
+        cudaFree(d_any);
+        if (h_any) cudaFreeHost(h_any);
+    }
+
+    size_t fixed_smem() const { return tail_fixed_smem<T, NT>(depth - tl); }
+
+    int init(const tmg_level_desc *lv, int nl, long long batch, const tmg_plan_opts &opts)
+    {
+        depth = nl;
+        B = batch;
+        o = opts;
+        if (o.gamma < 1) o.gamma = 1;
+        for (int l = 0; l < nl; ++l) {
+            n.push_back(lv[l].n_slabs);
+            L.push_back(make_level<T, NT>(lv[l]));
+        }
+        for (int l = 0; l + 1 < nl; ++l)
+            if (n[l + 1] != n[l] / 2 || n[l] % 2)
+                return fail(TMG_E_ARG, "level %d: %lld slabs does not coarsen to %lld", l, n[l], n[l + 1]);
+        CK(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+        CK(cudaMalloc(&d_levels, sizeof(LevelC<T, NT>) * nl));
+        CK(cudaMemcpy(d_levels, L.data(), sizeof(LevelC<T, NT>) * nl, cudaMemcpyHostToDevice));
+
+        // choose the tail: the longest suffix of small levels that fits in smem
+        const size_t smem_cap = 200 * 1024;
+        long long tail_max = o.tail_max_slabs > 0 ? o.tail_max_slabs : (NT <= 2 ? 2048 : 1024);
+        auto store_of = [&](int l0) {
+            long long e = 0;
+            for (int l = l0; l < nl; ++l) e += 2 * n[l] * NT;
+            return e + (e & 1);
+        };
+        auto smem_of = [&](int l0) {
+            return tail_fixed_smem<T, NT>(nl - l0) + sizeof(T) * store_of(l0) +
+                   (l0 == 0 ? sizeof(double) * n[0] : 0);
+        };
+        tl = nl - 1;
+        for (int l = nl - 2; l >= 0; --l) {
+            if (n[l] <= tail_max && smem_of(l) <= smem_cap) tl = l;
+            else break;
+        }
+        store_elems = store_of(tl);
+        tail_smem = smem_of(tl) <= smem_cap;
+        tail_smem_bytes = tail_smem ? smem_of(tl) : fixed_smem();
+        if (!tail_smem)
+            CK(cudaMalloc(&gstore, (sizeof(T) * store_elems + sizeof(double) * (tl == 0 ? n[0] : 0)) * B + 64));
+        auto tk = tail_kernel<T, NT, SP>;
+        CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem_bytes));
+
+        uA.assign(nl, nullptr);
+        uB.assign(nl, nullptr);
+        fl.assign(nl, nullptr);
+        for (int l = 0; l <= tl && l < nl; ++l) {
+            const size_t bytes = sizeof(T) * n[l] * NT * B;
+            if (l > 0) {
+                CK(cudaMalloc(&uA[l], bytes));
+                CK(cudaMalloc(&fl[l], bytes));
+            }
+            if (l < tl) CK(cudaMalloc(&uB[l], bytes));
+        }
+        // norm machinery (finest level)
+        leaf_rows0 = leaf_rows_for(n[0]);
+        if (leaf_rows0) {
+            nleaves = n[0] / (32LL * leaf_rows0);
+            CK(cudaMalloc(&leaves, sizeof(double) * nleaves * B));
+        }
+        CK(cudaMalloc(&sqbuf, sizeof(double) * n[0] * B));
+        CK(cudaMalloc(&d_st, sizeof(ProbState) * B));
+        CK(cudaMalloc(&d_floor, sizeof(double) * B));
+        CK(cudaMalloc(&d_active, sizeof(int) * B));
+        CK(cudaMalloc(&d_any, sizeof(int) * 4));
+        CK(cudaHostAlloc(&h_any, sizeof(int) * 4, cudaHostAllocDefault));
+
+        targ = TailArgs<T, NT>{};
+        targ.levels = d_levels;
+        targ.l0 = tl;
+        targ.depth = nl;
+        long long off = 0;
+        for (int l = tl; l < nl; ++l) {
+            targ.n[l] = n[l];
+            targ.off[l] = off;
+            off += 2 * n[l] * NT;
+        }
+        targ.store_elems = store_elems;
+        targ.gstore = gstore;
+        targ.in_smem = tail_smem;
+        targ.nu1 = o.nu1;
+        targ.nu2 = o.nu2;
+        targ.gamma = o.gamma;
+        targ.dot_variant = o.dot_variant;
+        return 0;
+    }
+
+    // one cycle's launches (multigrid.py:263-330 for gamma = 1)
+    int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s)
+    {
+        const T *fL = l == 0 ? (const T *)f0 : fl[l];
+        // down
+        {
+            StreamArgs<T> a = stream_args<T>(n[l], B, 1);
+            a.f = fL;
+            const bool zero = (l > 0) && first_visit;
+            a.u_in = l == 0 ? (const T *)u0 : (zero ? nullptr : uA[l]);
+            a.u_out = uB[l];
+            a.fc = fl[l + 1];
+            a.active = d_active;
+            a.flags = SF_RESTRICT | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
+            if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+            CKR((launch_stream<T, NT, SP, false>(L[l], a, o.nu1, s)));
+            ++kernels_per_cycle;
+        }
+        // coarse-grid correction
+        if (l + 1 == tl) {
+            TailArgs<T, NT> t = targ;
+            t.f_in = fl[tl];
+            t.u_in = nullptr;
+            t.u_out = uA[tl];
+            t.full = 0;
+            t.n_cycles = (tl == depth - 1) ? 1 : o.gamma;
+            t.active = d_active;
+            tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
+            CK(cudaGetLastError());
+            ++kernels_per_cycle;
+        } else {
+            for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s));
+        }
+        // up
+        {
+            const bool leaf = norm && leaf_rows0 > 0;
+            StreamArgs<T> a = stream_args<T>(n[l], B, leaf ? leaf_rows0 : 1);
+            a.f = fL;
+            a.u_in = uB[l];
+            a.uc = uA[l + 1];
+            a.u_out = l == 0 ? (T *)u0 : uA[l];
+            a.active = d_active;
+            a.flags = SF_PROLONG | SF_WRITE_U;
+            if (norm) {
+                if (leaf) { a.flags |= SF_NORM_LEAF; a.leaf_out = leaves; }
+                else { a.flags |= SF_NORM_SQ; a.sq_out = sqbuf; }
+            }
+            if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
+            CKR((launch_stream<T, NT, SP, true>(L[l], a, o.nu2, s)));
+            ++kernels_per_cycle;
+        }
+        return 0;
+    }
+
+    int enqueue_finalize(int mode, double eps, cudaStream_t s)
+    {
+        if (leaf_rows0)
+            finalize_leaves_kernel<<<(unsigned)B, 1024, 0, s>>>(leaves, nleaves, d_st, d_hist, hist_stride,
+                                                               d_floor, eps, mode);
+        else
+            finalize_sq_kernel<<<(unsigned)B, 1024, 0, s>>>(sqbuf, n[0], d_st, d_hist, hist_stride, d_floor,
+                                                           eps, mode, nullptr);
+        CK(cudaGetLastError());
+        active_flags_kernel<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(d_st, d_active, d_any, (int)B);
+        CK(cudaGetLastError());
+        kernels_per_cycle += 2;
+        return 0;
+    }
+
+    int enqueue_cycle(const void *f, void *u, bool norm, double eps, cudaStream_t s)
+    {
+        kernels_per_cycle = 0;
+        CKR(enqueue_level(0, f, u, true, norm, s));
+        if (norm) {
+            CK(cudaMemsetAsync(d_any, 0, sizeof(int), s));
+            CKR(enqueue_finalize(1, eps, s));
+        }
+        return 0;
+    }
+
+    int run_cycle(const void *f, void *u, bool norm, double eps, cudaStream_t s)
+    {
+        if (!o.use_graph) return enqueue_cycle(f, u, norm, eps, s);
+        if (!gexec || g_f != f || g_u != u || g_norm != norm || g_eps != eps) {
+            if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            int rc = enqueue_cycle(f, u, norm, eps, s);
+            cudaError_t ce = cudaStreamEndCapture(s, &g);
+            if (rc) return rc;
+            CK(ce);
+            CK(cudaGraphInstantiate(&gexec, g, 0));
+            cudaGraphDestroy(g);
+            g_f = f; g_u = u; g_norm = norm; g_eps = eps;
+        }
+        CK(cudaGraphLaunch(gexec, s));
+        return 0;
+    }
+
+    int enter(cudaStream_t user)
+    {
+        CK(cudaEventRecord(ev_in, user));
+        CK(cudaStreamWaitEvent(ps, ev_in, 0));
+        return 0;
+    }
+    int leave(cudaStream_t user)
+    {
+        CK(cudaEventRecord(ev_out, ps));
+        CK(cudaStreamWaitEvent(user, ev_out, 0));
+        return 0;
+    }
+
+    int cycles(const void *f, void *u, int nc, cudaStream_t user) override
+    {
+        CKR(enter(user));
+        CKR(cycles_on(f, u, nc, ps));
+        return leave(user);
+    }
+    int solve(const void *f, void *u, const double *floor_, double eps, int max_iters,
+              cudaStream_t user) override
+    {
+        CKR(enter(user));
+        CKR(solve_on(f, u, floor_, eps, max_iters, ps));
+        return leave(user);
+    }
+
+    int cycles_on(const void *f, void *u, int nc, cudaStream_t s)
+    {
+        if (tl == 0) {
+            TailArgs<T, NT> t = targ;
+            t.f_in = (const T *)f;
+            t.u_in = (const T *)u;
+            t.u_out = (T *)u;
+            t.full = 0;
+            t.n_cycles = nc;
+            t.active = nullptr;
+            tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
+            CK(cudaGetLastError());
+            return 0;
+        }
+        CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));  // all active (nonzero)
+        for (int c = 0; c < nc; ++c) CKR(run_cycle(f, u, false, 0.0, s));
+        return 0;
+    }
+
+    int solve_on(const void *f, void *u, const double *floor_, double eps, int max_iters,
+                 cudaStream_t s)
+    {
+        if (max_iters < 1) return fail(TMG_E_ARG, "max_iters must be >= 1");
+        if (max_iters + 1 > hist_stride) {
+            cudaFree(d_hist);
+            hist_stride = max_iters + 1;
+            CK(cudaMalloc(&d_hist, sizeof(double) * hist_stride * B));
+            if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+        }
+        last_max_iters = max_iters;
+        CK(cudaMemcpyAsync(d_floor, floor_, sizeof(double) * B, cudaMemcpyHostToDevice, s));
+        std::vector<ProbState> init(B);
+        for (auto &p : init) { p.tol = 0; p.iters = 0; p.active = 1; p.max_iters = max_iters; p.converged = 0; }
+        CK(cudaMemcpyAsync(d_st, init.data(), sizeof(ProbState) * B, cudaMemcpyHostToDevice, s));
+        if (tl == 0) {
+            TailArgs<T, NT> t = targ;
+            t.f_in = (const T *)f;
+            t.u_in = (const T *)u;
+            t.u_out = (T *)u;
+            t.full = 1;
+            t.eps = eps;
+            t.floor_ = d_floor;
+            t.max_iters = max_iters;
+            t.hist = d_hist;
+            t.st = d_st;
+            t.active = nullptr;
+            tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
+            CK(cudaGetLastError());
+        } else {
+            // r0 = ||f - L u_init|| (norm_at before the loop, multigrid.py:478)
+            CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));
+            {
+                const bool leaf = leaf_rows0 > 0;
+                StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
+                a.f = (const T *)f;
+                a.u_in = (const T *)u;
+                a.flags = leaf ? SF_NORM_LEAF : SF_NORM_SQ;
+                a.leaf_out = leaves;
+                a.sq_out = sqbuf;
+                if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+                CKR((launch_stream<T, NT, SP, false>(L[0], a, 0, s)));
+            }
+            CK(cudaMemsetAsync(d_any, 0, sizeof(int), s));
+            CKR(enqueue_finalize(0, eps, s));
+            CK(cudaMemcpyAsync(h_any, d_any, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            int it = 0;
+            while (h_any[0] && it < max_iters) {
+                CKR(run_cycle(f, u, true, eps, s));
+                CK(cudaMemcpyAsync(h_any, d_any, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                ++it;
+            }
+        }
+        // results
+        std::vector<ProbState> st(B);
+        h_hist.resize((size_t)hist_stride * B);
+        CK(cudaMemcpyAsync(st.data(), d_st, sizeof(ProbState) * B, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_hist.data(), d_hist, sizeof(double) * hist_stride * B, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        h_it.resize(B);
+        h_conv.resize(B);
+        for (long long b = 0; b < B; ++b) {
+            h_it[b] = st[b].iters;
+            h_conv[b] = st[b].converged;
+        }
+        return 0;
+    }
+
+    int stats(int32_t *it, double *norms, int32_t *conv) const override
+    {
+        if (h_it.empty()) return fail(TMG_E_ARG, "no solve has run on this plan");
+        for (long long b = 0; b < B; ++b) {
+            if (it) it[b] = h_it[b];
+            if (conv) conv[b] = h_conv[b];
+            if (norms)
+                for (int k = 0; k <= last_max_iters; ++k)
+                    norms[b * (last_max_iters + 1) + k] = k <= h_it[b] ? h_hist[b * hist_stride + k] : 0.0;
+        }
+        return 0;
+    }
+
+    int info(int32_t *kpc, int32_t *sl, int32_t *t) const override
+    {
+        if (kpc) *kpc = kernels_per_cycle;
+        if (sl) *sl = tl;
+        if (t) *t = tl;
+        return 0;
+    }
+};
+
+template <typename T, int NT>
+int make_plan_sp(std::unique_ptr<PlanBase> &out, const tmg_level_desc *lv, int nl, long long B,
+                 const tmg_plan_opts &o)
+{
+    if (coupling_is_sparse(lv[0])) {
+        auto p = std::make_unique<Plan<T, NT, true>>();
+        CKR(p->init(lv, nl, B, o));
+        out = std::move(p);
+    } else {
+        auto p = std::make_unique<Plan<T, NT, false>>();
+        CKR(p->init(lv, nl, B, o));
+        out = std::move(p);
+    }
+    return 0;
+}
+
+template <typename T>
+int make_plan_t(std::unique_ptr<PlanBase> &out, const tmg_level_desc *lv, int nl, long long B,
+                const tmg_plan_opts &o)
+{
+    switch (lv[0].n_t) {
+    case 1: return make_plan_sp<T, 1>(out, lv, nl, B, o);
+    case 2: return make_plan_sp<T, 2>(out, lv, nl, B, o);
+    case 3: return make_plan_sp<T, 3>(out, lv, nl, B, o);
+    case 4: return make_plan_sp<T, 4>(out, lv, nl, B, o);
+    }
+    return fail(TMG_E_UNSUPPORTED, "n_t=%d", lv[0].n_t);
+}
+
+// ---------------------------------------------------------------------------
+// single-level entry points
+
+enum Op { OP_SWEEP, OP_RESID, OP_DOWN, OP_UP, OP_NORM };
+
+struct OpArgs {
+    const void *f, *u_in, *uc;
+    void *u_out, *aux;  // aux: r (RESID), f_coarse (DOWN)
+    double *sq;
+    long long batch;
+    int nu;
+    const int32_t *active;
+};
+
+template <typename T, int NT, bool SP>
+int run_op(Op op, const tmg_level_desc &d, const OpArgs &x, cudaStream_t s)
+{
+    const LevelC<T, NT> L = make_level<T, NT>(d);
+    const long long n = d.n_slabs;
+    StreamArgs<T> a = stream_args<T>(n, x.batch, 1);
+    a.f = (const T *)x.f;
+    a.u_in = (const T *)x.u_in;
+    a.active = x.active;
+    switch (op) {
+    case OP_SWEEP: {
+        if (x.nu == 0) {
+            if (x.u_in) CK(cudaMemcpyAsync(x.u_out, x.u_in, sizeof(T) * n * NT * x.batch, cudaMemcpyDeviceToDevice, s));
+            else CK(cudaMemsetAsync(x.u_out, 0, sizeof(T) * n * NT * x.batch, s));
+            return 0;
+        }
+        // chains of <= 4 fused sweeps; ping-pong through a scratch buffer
+        int left = x.nu;
+        const T *src = (const T *)x.u_in;
+        T *tmp = nullptr;
+        const int passes = (x.nu + 3) / 4;
+        if (passes > 1) CK(cudaMallocAsync(&tmp, sizeof(T) * n * NT * x.batch, s));
+        // make the last pass land in u_out
+        T *bufs[2] = {(T *)x.u_out, tmp};
+        int idx = (passes % 2 == 1) ? 0 : 1;
+        while (left > 0) {
+            const int k = std::min(4, left);
+            StreamArgs<T> b = a;
+            b.u_in = src;
+            b.u_out = bufs[idx];
+            b.flags = SF_WRITE_U | (src ? 0 : SF_ZERO_GUESS);
+            if (tma_ok<T, NT>(b, false)) b.flags |= SF_TMA;
+            CKR((launch_stream<T, NT, SP, false>(L, b, k, s)));
+            src = bufs[idx];
+            idx ^= 1;
+            left -= k;
+        }
+        if (tmp) CK(cudaFreeAsync(tmp, s));
+        return 0;
+    }
+    case OP_RESID:
+        a.r_out = (T *)x.aux;
+        a.flags = SF_WRITE_R;
+        if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+        return launch_stream<T, NT, SP, false>(L, a, 0, s);
+    case OP_DOWN:
+        a.u_out = (T *)x.u_out;
+        a.fc = (T *)x.aux;
+        a.flags = SF_RESTRICT | SF_WRITE_U | (x.u_in ? 0 : SF_ZERO_GUESS);
+        if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+        return launch_stream<T, NT, SP, false>(L, a, x.nu, s);
+    case OP_UP:
+        a.uc = (const T *)x.uc;
+        a.u_out = (T *)x.u_out;
+        a.flags = SF_PROLONG | SF_WRITE_U | (x.sq ? SF_NORM_SQ : 0);
+        a.sq_out = x.sq;
+        if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
+        return launch_stream<T, NT, SP, true>(L, a, x.nu, s);
+    case OP_NORM: {
+        double *sq = nullptr;
+        CK(cudaMallocAsync(&sq, sizeof(double) * n * x.batch, s));
+        a.sq_out = sq;
+        a.flags = SF_NORM_SQ;
+        if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+        int rc = launch_stream<T, NT, SP, false>(L, a, 0, s);
+        if (!rc) {
+            finalize_sq_kernel<<<(unsigned)x.batch, 1024, 0, s>>>(sq, n, nullptr, nullptr, 0, nullptr, 0.0, 0,
+                                                                (double *)x.aux);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) rc = fail((int)e, "finalize: %s", cudaGetErrorString(e));
+        }
+        cudaFreeAsync(sq, s);
+        return rc;
+    }
+    }
+    return fail(TMG_E_ARG, "bad op");
+}
+
+template <typename T>
+int run_op_t(Op op, const tmg_level_desc &d, const OpArgs &x, cudaStream_t s)
+{
+    const bool sp = coupling_is_sparse(d);
+#define TMG_CASE(NTV)                                                             \
+    case NTV:                                                                     \
+        return sp ? run_op<T, NTV, true>(op, d, x, s) : run_op<T, NTV, false>(op, d, x, s);
+    switch (d.n_t) {
+        TMG_CASE(1)
+        TMG_CASE(2)
+        TMG_CASE(3)
+        TMG_CASE(4)
+    }
+#undef TMG_CASE
+    return fail(TMG_E_UNSUPPORTED, "n_t=%d", d.n_t);
+}
+
+int run_op_any(int dtype, Op op, const tmg_level_desc *d, const OpArgs &x, void *stream)
+{
+    CKR(check_desc(d));
+    if (x.batch < 1) return fail(TMG_E_ARG, "batch must be >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == TMG_F64) return run_op_t<double>(op, *d, x, s);
+    if (dtype == TMG_F32) return run_op_t<float>(op, *d, x, s);
+    return fail(TMG_E_ARG, "unknown dtype %d", dtype);
+}
+
+template <typename T, int NT, bool SP>
+int coarse_op(const tmg_level_desc &d, const void *f, void *u, long long B, int method, int variant,
+              cudaStream_t s)
+{
+    if (method != 0) return fail(TMG_E_UNSUPPORTED, "scan coarse solve not built in this version");
+    const LevelC<T, NT> L = make_level<T, NT>(d);
+    coarse_serial_kernel<T, NT, SP><<<(unsigned)((B + 31) / 32), 32, 0, s>>>(L, (const T *)f, (T *)u, d.n_slabs,
+                                                                            (int)B, variant, nullptr);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// exported C ABI
+
+extern "C" {
+
+const char *tmg_last_error(void) { return g_err.c_str(); }
+
+int tmg_version(void) { return 100; }
+
+int tmg_device_check(int device)
+{
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, device));
+    if (p.major < 10) return fail(TMG_E_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                                  device, p.major, p.minor);
+    return 0;
+}
+
+int tmg_sweep(int dtype, const tmg_level_desc *lev, const void *f, const void *u_in, void *u_out,
+              int64_t batch, int nu, const int32_t *active, void *stream)
+{
+    if (nu < 0) return fail(TMG_E_ARG, "sweep count must be >= 0, got %d", nu);
+    if (lev && !(lev->omega > 0.0 && lev->omega < 2.0))
+        return fail(TMG_E_ARG, "damping must lie in (0, 2), got %g", lev->omega);
+    if (u_in && u_in == u_out) return fail(TMG_E_ARG, "u_in and u_out must not alias");
+    OpArgs x{f, u_in, nullptr, u_out, nullptr, nullptr, batch, nu, active};
+    return run_op_any(dtype, OP_SWEEP, lev, x, stream);
+}
+
+int tmg_residual(int dtype, const tmg_level_desc *lev, const void *f, const void *u, void *r,
+                 int64_t batch, void *stream)
+{
+    OpArgs x{f, u, nullptr, nullptr, r, nullptr, batch, 0, nullptr};
+    return run_op_any(dtype, OP_RESID, lev, x, stream);
+}
+
+int tmg_down(int dtype, const tmg_level_desc *lev, const void *f, const void *u_in, void *u_out,
+             void *f_coarse, int64_t batch, int nu1, const int32_t *active, void *stream)
+{
+    if (u_in && u_in == u_out) return fail(TMG_E_ARG, "u_in and u_out must not alias");
+    OpArgs x{f, u_in, nullptr, u_out, f_coarse, nullptr, batch, nu1, active};
+    return run_op_any(dtype, OP_DOWN, lev, x, stream);
+}
+
+int tmg_up(int dtype, const tmg_level_desc *lev, const void *f, const void *u_in, const void *u_coarse,
+           void *u_out, double *sq_out, int64_t batch, int nu2, const int32_t *active, void *stream)
+{
+    if (u_in == u_out) return fail(TMG_E_ARG, "u_in and u_out must not alias");
+    OpArgs x{f, u_in, u_coarse, u_out, nullptr, sq_out, batch, nu2, active};
+    return run_op_any(dtype, OP_UP, lev, x, stream);
+}
+
+int tmg_coarse_solve(int dtype, const tmg_level_desc *lev, const void *f, void *u, int64_t batch,
+                     int method, int dot_variant, void *stream)
+{
+    CKR(check_desc(lev));
+    if (dot_variant == 0 && lev->n_t > 4) return fail(TMG_E_UNSUPPORTED, "no calibrated dgemv tree for n_t > 4");
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool sp = coupling_is_sparse(*lev);
+#define TMG_CC(T, NTV) \
+    case NTV: return sp ? coarse_op<T, NTV, true>(*lev, f, u, batch, method, dot_variant, s) \
+                        : coarse_op<T, NTV, false>(*lev, f, u, batch, method, dot_variant, s);
+    if (dtype == TMG_F64) {
+        switch (lev->n_t) { TMG_CC(double, 1) TMG_CC(double, 2) TMG_CC(double, 3) TMG_CC(double, 4) }
+    } else if (dtype == TMG_F32) {
+        switch (lev->n_t) { TMG_CC(float, 1) TMG_CC(float, 2) TMG_CC(float, 3) TMG_CC(float, 4) }
+    }
+#undef TMG_CC
+    return fail(TMG_E_ARG, "bad dtype/n_t");
+}
+
+int tmg_resid_norm(int dtype, const tmg_level_desc *lev, const void *f, const void *u, double *norms_out,
+                   int64_t batch, void *stream)
+{
+    OpArgs x{f, u, nullptr, nullptr, norms_out, nullptr, batch, 0, nullptr};
+    return run_op_any(dtype, OP_NORM, lev, x, stream);
+}
+
+int tmg_plan_create(tmg_plan **plan, const tmg_level_desc *levels, int n_levels, int64_t batch,
+                    const tmg_plan_opts *opts)
+{
+    if (!plan || !levels || !opts) return fail(TMG_E_ARG, "NULL argument");
+    *plan = nullptr;
+    if (n_levels < 2 || n_levels > MAXLEV) return fail(TMG_E_ARG, "need 2..%d levels, got %d", MAXLEV, n_levels);
+    if (batch < 1) return fail(TMG_E_ARG, "batch must be >= 1");
+    for (int l = 0; l < n_levels; ++l) {
+        CKR(check_desc(&levels[l]));
+        if (levels[l].n_t != levels[0].n_t) return fail(TMG_E_ARG, "levels disagree on n_t");
+    }
+    if (opts->nu1 < 0 || opts->nu2 < 0 || opts->nu1 + opts->nu2 < 1)
+        return fail(TMG_E_ARG, "need nu1, nu2 >= 0 with nu1 + nu2 >= 1");
+    if (opts->nu1 > 4 || opts->nu2 > 4) return fail(TMG_E_UNSUPPORTED, "nu > 4 not supported");
+    if (opts->dot_variant == 0 && levels[0].n_t > 4) return fail(TMG_E_UNSUPPORTED, "dgemv tree");
+    auto p = std::make_unique<tmg_plan>();
+    int rc;
+    if (opts->dtype == TMG_F64) rc = make_plan_t<double>(p->impl, levels, n_levels, batch, *opts);
+    else if (opts->dtype == TMG_F32) rc = make_plan_t<float>(p->impl, levels, n_levels, batch, *opts);
+    else return fail(TMG_E_ARG, "unknown dtype");
+    if (rc) return rc;
+    *plan = p.release();
+    return 0;
+}
+
+int tmg_plan_destroy(tmg_plan *plan)
+{
+    delete plan;
+    return 0;
+}
+
+int tmg_plan_cycles(tmg_plan *plan, const void *f, void *u, int n_cycles, void *stream)
+{
+    if (!plan) return fail(TMG_E_ARG, "NULL plan");
+    return plan->impl->cycles(f, u, n_cycles, (cudaStream_t)stream);
+}
+
+int tmg_plan_solve(tmg_plan *plan, const void *f, void *u, const double *floor_per_problem, double eps,
+                   int max_iters, void *stream)
+{
+    if (!plan) return fail(TMG_E_ARG, "NULL plan");
+    if (!(eps > 0.0 && eps < 1.0)) return fail(TMG_E_ARG, "eps must lie in (0, 1)");
+    return plan->impl->solve(f, u, floor_per_problem, eps, max_iters, (cudaStream_t)stream);
+}
+
+int tmg_plan_stats(const tmg_plan *plan, int32_t *iterations, double *norms, int32_t *converged)
+{
+    if (!plan) return fail(TMG_E_ARG, "NULL plan");
+    return plan->impl->stats(iterations, norms, converged);
+}
+
+int tmg_plan_info(const tmg_plan *plan, int32_t *kernels_per_cycle, int32_t *stream_levels,
+                  int32_t *tail_level)
+{
+    if (!plan) return fail(TMG_E_ARG, "NULL plan");
+    return plan->impl->info(kernels_per_cycle, stream_levels, tail_level);
+}
+
+}  // extern "C"

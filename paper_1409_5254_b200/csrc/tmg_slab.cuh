@@ -1,0 +1,357 @@
+// Per-slab arithmetic of the time-multigrid hot path, sm_100a.
+//
+// Every function here reproduces the float64 operation order of the
+// reference (arxiv/paper_1409_5254, pkg/src/timemg/multigrid.py and dg.py)
+// with explicitly rounded IEEE operations (__dmul_rn / __dadd_rn / __dsub_rn /
+// __ddiv_rn; the library is also compiled with -fmad=false), so the GPU
+// iterates are bit-identical to the reference's:
+//   bmat           _block_apply  multigrid.py:145-155 (j ascending, mul then add)
+//   residual       _residual_slab multigrid.py:158-165 : ((A u) + f) + N u_prev
+//   lu_solve       BlockLU.solve_rows dg.py:153-168 (perm, forward, backward, /)
+//   sweep          _sweep_slab   multigrid.py:168-180 : (LU^-1 r) * omega + u
+//   restrict_part  _restrict_slab multigrid.py:183-185 : R1 r_2c + R2 r_2c+1
+//   prolong_part   _prolong_add_slab multigrid.py:188-190 : u += R^T u_c
+//   sqnorm         _sqnorm_slab  multigrid.py:193-197
+//   blas_dot       `coupling @ x` in _forward_substitute multigrid.py:205
+//
+// Coupling.  For the default radau_lagrange basis the coupling block
+// N = outer(eval_start, eval_end) has nonzeros only in row 0 (eval_start = e0)
+// -- the "sparse" path: a slab needs ONE scalar from its predecessor,
+// s = sum_j N[0,j] u_prev[j] (same order as the reference's row-0 product),
+// plus the sign bits of u_prev, which fix the sign of the exact zeros the
+// reference adds to rows >= 1 (r_i + (+-0)).  That keeps the result bitwise
+// identical including signed zeros.  Any other coupling (scaled_legendre)
+// takes the "general" path that exchanges the whole predecessor slab.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tmg {
+
+template <typename T> struct FP;
+template <> struct FP<double> {
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+    static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+    static __device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
+    static __device__ __forceinline__ unsigned sbit(double x) {
+        return (unsigned)((unsigned long long)__double_as_longlong(x) >> 63);
+    }
+    static __device__ __forceinline__ double zero(bool neg) { return neg ? -0.0 : 0.0; }
+};
+template <> struct FP<float> {
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+    static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+    static __device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+    static __device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+    static __device__ __forceinline__ unsigned sbit(float x) { return (unsigned)__float_as_uint(x) >> 31; }
+    static __device__ __forceinline__ float zero(bool neg) { return neg ? -0.0f : 0.0f; }
+};
+
+// Per-level constants in the compute type (kernel parameter / shared memory).
+template <typename T, int NT> struct LevelC {
+    T A[NT * NT];   // minus_step_matrix  (dg.py:213-215)
+    T C[NT * NT];   // coupling           (dg.py:236)
+    T lu[NT * NT];  // BlockLU.lu         (dg.py:145)
+    T R1[NT * NT];  // Level.r1           (transfers.py:16-37)
+    T R2[NT * NT];  // Level.r2
+    T omega;        // resolve_damping(alpha(tau))
+    int perm[NT];   // BlockLU.perm       (dg.py:148-151)
+    unsigned cneg[NT];  // sign bits of coupling row i (sparse path)
+    int has_transfer;
+};
+
+// What a slab needs from its predecessor.
+template <typename T, int NT, bool SPARSE> struct Cpl;
+template <typename T, int NT> struct Cpl<T, NT, true> {
+    T s;         // sum_j C[0,j] u_prev[j]
+    unsigned m;  // sign bits of u_prev
+};
+template <typename T, int NT> struct Cpl<T, NT, false> {
+    T u[NT];
+};
+
+template <typename T, int NT>
+__device__ __forceinline__ void bmat(const T *M, const T (&x)[NT], T (&o)[NT])
+{
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        T a = FP<T>::mul(M[i * NT], x[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(M[i * NT + j], x[j]));
+        o[i] = a;
+    }
+}
+
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ Cpl<T, NT, SPARSE> make_cpl(const LevelC<T, NT> &L, const T (&u)[NT])
+{
+    Cpl<T, NT, SPARSE> c;
+    if constexpr (SPARSE) {
+        T a = FP<T>::mul(L.C[0], u[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(L.C[j], u[j]));
+        c.s = a;
+        unsigned m = 0;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) m |= FP<T>::sbit(u[j]) << j;
+        c.m = m;
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) c.u[j] = u[j];
+    }
+    return c;
+}
+
+template <typename T> __device__ __forceinline__ T shfl_up_t(T v, int d)
+{
+    return __shfl_up_sync(0xffffffffu, v, d);
+}
+template <typename T> __device__ __forceinline__ T shfl_t(T v, int src)
+{
+    return __shfl_sync(0xffffffffu, v, src);
+}
+
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ Cpl<T, NT, SPARSE> cpl_shfl_up(const Cpl<T, NT, SPARSE> &c)
+{
+    Cpl<T, NT, SPARSE> o;
+    if constexpr (SPARSE) {
+        o.s = shfl_up_t(c.s, 1);
+        o.m = shfl_up_t(c.m, 1);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) o.u[j] = shfl_up_t(c.u[j], 1);
+    }
+    return o;
+}
+
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ Cpl<T, NT, SPARSE> cpl_shfl(const Cpl<T, NT, SPARSE> &c, int src)
+{
+    Cpl<T, NT, SPARSE> o;
+    if constexpr (SPARSE) {
+        o.s = shfl_t(c.s, src);
+        o.m = shfl_t(c.m, src);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) o.u[j] = shfl_t(c.u[j], src);
+    }
+    return o;
+}
+
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ void cpl_zero(Cpl<T, NT, SPARSE> &c)
+{
+    if constexpr (SPARSE) {
+        c.s = T(0);
+        c.m = 0;
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) c.u[j] = T(0);
+    }
+}
+
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ void cpl_select(Cpl<T, NT, SPARSE> &dst, const Cpl<T, NT, SPARSE> &src,
+                                           bool take)
+{
+    if constexpr (SPARSE) {
+        dst.s = take ? src.s : dst.s;
+        dst.m = take ? src.m : dst.m;
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dst.u[j] = take ? src.u[j] : dst.u[j];
+    }
+}
+
+// r = ((A u) + f) [+ N u_prev if has_prev]   (multigrid.py:159-165)
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ void residual(const LevelC<T, NT> &L, const T (&u)[NT], const T (&f)[NT],
+                                         const Cpl<T, NT, SPARSE> &p, bool has_prev, T (&r)[NT])
+{
+    bmat<T, NT>(L.A, u, r);
+#pragma unroll
+    for (int i = 0; i < NT; ++i) r[i] = FP<T>::add(r[i], f[i]);
+    if constexpr (SPARSE) {
+        T r0 = FP<T>::add(r[0], p.s);
+        r[0] = has_prev ? r0 : r[0];
+        const unsigned full = (1u << NT) - 1u;
+#pragma unroll
+        for (int i = 1; i < NT; ++i) {
+            // the reference adds sum_j (+-0 * u_prev[j]): -0 iff every product is -0
+            T ri = FP<T>::add(r[i], FP<T>::zero(((p.m ^ L.cneg[i]) & full) == full));
+            r[i] = has_prev ? ri : r[i];
+        }
+    } else {
+        T c[NT];
+        bmat<T, NT>(L.C, p.u, c);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            T ri = FP<T>::add(r[i], c[i]);
+            r[i] = has_prev ? ri : r[i];
+        }
+    }
+}
+
+// y = LU^-1 r  (dg.py:153-168)
+template <typename T, int NT>
+__device__ __forceinline__ void lu_solve(const LevelC<T, NT> &L, const T (&r)[NT], T (&y)[NT])
+{
+    if constexpr (NT == 1) {
+        y[0] = FP<T>::div(r[0], L.lu[0]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            T v = r[0];
+#pragma unroll
+            for (int q = 1; q < NT; ++q) v = (L.perm[i] == q) ? r[q] : v;
+            y[i] = v;
+        }
+#pragma unroll
+        for (int i = 1; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < i; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+#pragma unroll
+        for (int i = NT - 1; i >= 0; --i) {
+#pragma unroll
+            for (int j = i + 1; j < NT; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+            y[i] = FP<T>::div(y[i], L.lu[i * NT + i]);
+        }
+    }
+}
+
+// one damped block-Jacobi update of slab n in place (multigrid.py:169-180)
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ void sweep(const LevelC<T, NT> &L, T (&u)[NT], const T (&f)[NT],
+                                      const Cpl<T, NT, SPARSE> &p, bool has_prev)
+{
+    T r[NT], c[NT];
+    residual<T, NT, SPARSE>(L, u, f, p, has_prev, r);
+    lu_solve<T, NT>(L, r, c);
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        c[i] = FP<T>::mul(c[i], L.omega);
+        u[i] = FP<T>::add(c[i], u[i]);
+    }
+}
+
+// lane-selected transfer product: odd ? R2 r : R1 r   (multigrid.py:184-185)
+template <typename T, int NT>
+__device__ __forceinline__ void restrict_part(const LevelC<T, NT> &L, const T (&r)[NT], bool odd,
+                                              T (&o)[NT])
+{
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        T a = FP<T>::mul(odd ? L.R2[i * NT] : L.R1[i * NT], r[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j)
+            a = FP<T>::add(a, FP<T>::mul(odd ? L.R2[i * NT + j] : L.R1[i * NT + j], r[j]));
+        o[i] = a;
+    }
+}
+
+// u += (odd ? R2 : R1)^T uc   (multigrid.py:189-190)
+template <typename T, int NT>
+__device__ __forceinline__ void prolong_part(const LevelC<T, NT> &L, const T (&uc)[NT], bool odd,
+                                             T (&u)[NT])
+{
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        T a = FP<T>::mul(odd ? L.R2[i] : L.R1[i], uc[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(odd ? L.R2[j * NT + i] : L.R1[j * NT + i], uc[j]));
+        u[i] = FP<T>::add(u[i], a);
+    }
+}
+
+template <typename T, int NT> __device__ __forceinline__ T sqnorm(const T (&r)[NT])
+{
+    T a = FP<T>::mul(r[0], r[0]);
+#pragma unroll
+    for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(r[j], r[j]));
+    return a;
+}
+
+// One row of `coupling @ x` as numpy/OpenBLAS computes it (multigrid.py:205).
+// variant 0: trees measured on the golden host (OpenBLAS 0.3.30); 1: sequential.
+template <typename T, int NT>
+__device__ __forceinline__ T blas_dot(const T *a, const T (&x)[NT], int variant)
+{
+    T t;
+    if (variant == 1 || NT > 4) {
+        t = FP<T>::mul(a[0], x[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) t = FP<T>::add(t, FP<T>::mul(a[j], x[j]));
+    } else if constexpr (NT == 1) {
+        t = FP<T>::mul(a[0], x[0]);
+    } else if constexpr (NT == 2) {
+        t = FP<T>::fma(a[0], x[0], FP<T>::mul(a[1], x[1]));
+    } else if constexpr (NT == 3) {
+        t = FP<T>::fma(a[2], x[2], FP<T>::fma(a[0], x[0], FP<T>::mul(a[1], x[1])));
+    } else {
+        T p0 = FP<T>::mul(a[0], x[0]), p1 = FP<T>::mul(a[1], x[1]);
+        T p2 = FP<T>::mul(a[2], x[2]), p3 = FP<T>::mul(a[3 % NT], x[3 % NT]);
+        t = FP<T>::add(FP<T>::add(p0, p2), FP<T>::add(p1, p3));
+    }
+    return FP<T>::add(t, T(0));
+}
+
+// ---- slab I/O helpers ------------------------------------------------------
+
+template <typename T, int NT>
+__device__ __forceinline__ void load_slab(const T *p, T (&x)[NT])
+{
+    if constexpr (sizeof(T) == 8 && NT % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < NT; j += 2) {
+            double2 v = *reinterpret_cast<const double2 *>(p + j);
+            x[j] = v.x;
+            x[j + 1] = v.y;
+        }
+    } else if constexpr (sizeof(T) == 4 && NT == 4) {
+        float4 v = *reinterpret_cast<const float4 *>(p);
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else if constexpr (sizeof(T) == 4 && NT == 2) {
+        float2 v = *reinterpret_cast<const float2 *>(p);
+        x[0] = v.x; x[1] = v.y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) x[j] = p[j];
+    }
+}
+
+template <typename T, int NT>
+__device__ __forceinline__ void store_slab(T *p, const T (&x)[NT])
+{
+    if constexpr (sizeof(T) == 8 && NT % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < NT; j += 2) *reinterpret_cast<double2 *>(p + j) = make_double2(x[j], x[j + 1]);
+    } else if constexpr (sizeof(T) == 4 && NT == 4) {
+        *reinterpret_cast<float4 *>(p) = make_float4(x[0], x[1], x[2], x[3]);
+    } else if constexpr (sizeof(T) == 4 && NT == 2) {
+        *reinterpret_cast<float2 *>(p) = make_float2(x[0], x[1]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) p[j] = x[j];
+    }
+}
+
+template <typename T, int NT>
+__device__ __forceinline__ void load_slab_scalar(const T *p, T (&x)[NT])
+{
+#pragma unroll
+    for (int j = 0; j < NT; ++j) x[j] = p[j];
+}
+
+template <typename T, int NT> __device__ __forceinline__ void zero_slab(T (&x)[NT])
+{
+#pragma unroll
+    for (int j = 0; j < NT; ++j) x[j] = T(0);
+}
+
+}  // namespace tmg

@@ -1,0 +1,302 @@
+"""GPU-backed drop-in for the reference solver API (pkg/src/timemg/multigrid.py).
+
+Same names, arguments, defaults, return values and errors as the reference:
+  block_jacobi_sweep(ops, u, f, omega, nu=1)           multigrid.py:208-220
+  two_grid_cycle(hier, level, u, f, config=None)       multigrid.py:355-363
+  v_cycle(hier, u, f, config=None)                     multigrid.py:366-375
+  solve(hier, f, u_init=None, config=None)             multigrid.py:509-531
+  measure_convergence_factor(hier, config=None)        multigrid.py:534-544
+  random_initial_guess(hier, seed)                     multigrid.py:503-506
+plus ``solve_batched`` (B independent right-hand sides sharing one operator,
+each stopping at its own iteration count) and the W-cycle via
+``CycleConfig(cycle="W")``.
+
+Arrays may be numpy (host; results come back as numpy) or torch CUDA tensors
+(device-resident; results stay on the device).  Every numeric step runs in the
+sm_100a kernels behind the C ABI; there is no CPU fallback.  ``hier`` may be
+this package's TimeHierarchy or the reference's own (duck-typed: ``levels``
+with ``n_steps``, ``tau``, ``ops``, ``r1``, ``r2``; ``basis``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _native as nat
+from .hierarchy import CycleConfig, SolveStats, depth_of, level_omegas, max_ratio
+
+_COARSE = {"serial": 0, "scan": 1, "auto": 2}
+# levels with at most this many slabs per problem run in the single-CTA engine
+# (0 = library default); exposed for tests of split invariance
+TAIL_MAX = 0
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("timemg_b200 needs a CUDA device (B200, sm_100a); there is no CPU path")
+    return torch
+
+
+def _dev(x, dtype_np=np.float64):
+    """(device tensor, was_torch).  numpy input is copied host->device."""
+    torch = _torch()
+    tdt = torch.float64 if dtype_np == np.float64 else torch.float32
+    if torch.is_tensor(x):
+        t = x.to(device="cuda", dtype=tdt).contiguous()
+        return t, True
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=dtype_np)).to("cuda"), False
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _out(t, was_torch):
+    if was_torch:
+        return t
+    return t.cpu().numpy()
+
+
+class DevicePlan:
+    """A tmg_plan: level constants, per-level device buffers, launch schedule."""
+
+    def __init__(self, hier, level0: int, depth: int, omegas, config: CycleConfig, batch: int,
+                 dtype: int = nat.F64, use_graph: bool = True):
+        lib = nat.load()
+        levels = hier.levels[level0:level0 + depth]
+        descs = (nat.LevelDesc * depth)()
+        for i, lev in enumerate(levels):
+            last = i + 1 == depth
+            descs[i] = nat.level_desc(lev.ops, lev.n_steps, omegas[i],
+                                      None if last else lev.r1, None if last else lev.r2)
+        self.depth = depth
+        self.batch = batch
+        self.n0 = levels[0].n_steps
+        self.n_t = levels[0].ops.n_t
+        self.dtype = dtype
+        opts = nat.PlanOpts(dtype, config.nu1, config.nu2, 2 if config.cycle == "W" else 1,
+                            _COARSE[config.coarse], int(config.dot_variant), int(use_graph),
+                            int(TAIL_MAX))
+        self._h = ctypes.c_void_p()
+        nat.check(lib.tmg_plan_create(ctypes.byref(self._h), descs, depth, batch, ctypes.byref(opts)),
+                  "tmg_plan_create")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and nat._lib is not None:
+            nat._lib.tmg_plan_destroy(h)
+            self._h = None
+
+    def cycles(self, f_dev, u_dev, n_cycles: int = 1):
+        nat.check(nat.load().tmg_plan_cycles(self._h, _ptr(f_dev), _ptr(u_dev), int(n_cycles),
+                                             _stream()), "tmg_plan_cycles")
+
+    def solve(self, f_dev, u_dev, floors, eps: float, max_iters: int):
+        floors = np.ascontiguousarray(floors, dtype=np.float64)
+        nat.check(nat.load().tmg_plan_solve(
+            self._h, _ptr(f_dev), _ptr(u_dev),
+            floors.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(eps), int(max_iters),
+            _stream()), "tmg_plan_solve")
+        it = np.zeros(self.batch, dtype=np.int32)
+        conv = np.zeros(self.batch, dtype=np.int32)
+        norms = np.zeros(self.batch * (max_iters + 1))
+        nat.check(nat.load().tmg_plan_stats(
+            self._h, it.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            conv.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), "tmg_plan_stats")
+        norms = norms.reshape(self.batch, max_iters + 1)
+        return it, norms, conv
+
+    def info(self):
+        k = ctypes.c_int32()
+        s = ctypes.c_int32()
+        t = ctypes.c_int32()
+        nat.check(nat.load().tmg_plan_info(self._h, ctypes.byref(k), ctypes.byref(s),
+                                           ctypes.byref(t)))
+        return {"kernels_per_cycle": k.value, "tail_level": t.value}
+
+
+def get_plan(hier, level0, depth, omegas, config, batch, dtype=nat.F64):
+    key = (level0, depth, tuple(omegas), config.nu1, config.nu2, config.cycle, config.coarse,
+           config.dot_variant, batch, dtype, TAIL_MAX)
+    cache = hier.__dict__.setdefault("_tmg_plans", {})
+    plan = cache.get(key)
+    if plan is None:
+        if len(cache) > 8:
+            cache.clear()
+        plan = DevicePlan(hier, level0, depth, omegas, config, batch, dtype)
+        cache[key] = plan
+    return plan
+
+
+# ---------------------------------------------------------------------------
+# reference API
+
+
+def random_initial_guess(hier, seed: int) -> np.ndarray:
+    """Uniform [0, 1) coefficients (multigrid.py:503-506)."""
+    rng = np.random.default_rng(seed)
+    return rng.random((hier.finest.n_steps, hier.finest.ops.n_t))
+
+
+def block_jacobi_sweep(ops, u, f, omega: float, nu: int = 1):
+    """nu damped block-Jacobi sweeps on the GPU (multigrid.py:208-220)."""
+    if not 0.0 < omega < 2.0:
+        raise ValueError(f"damping must lie in (0, 2), got {omega}")
+    if nu < 0:
+        raise ValueError(f"sweep count must be >= 0, got {nu}")
+    ud, was_t = _dev(u)
+    fd, _ = _dev(f)
+    out = _torch().empty_like(ud)
+    n = ud.shape[0]
+    d = nat.level_desc(ops, n, omega)
+    nat.check(nat.load().tmg_sweep(nat.F64, ctypes.byref(d), _ptr(fd), _ptr(ud), _ptr(out), 1,
+                                   int(nu), None, _stream()), "tmg_sweep")
+    return _out(out, was_t)
+
+
+def _cycle_api(hier, level, depth_total, u, f, config):
+    ud, was_t = _dev(u)
+    fd, _ = _dev(f)
+    omegas = level_omegas(hier, config, depth_total)[level:]
+    plan = get_plan(hier, level, depth_total - level, omegas, config, 1)
+    out = ud.clone()
+    plan.cycles(fd, out, 1)
+    return _out(out, was_t)
+
+
+def two_grid_cycle(hier, level: int, u, f, config: CycleConfig = None):
+    """Pre-smooth, restrict, exact coarse solve, prolongate, post-smooth
+    (multigrid.py:355-363)."""
+    config = config or CycleConfig()
+    if level + 1 >= len(hier.levels):
+        raise ValueError(f"level {level} has no coarser neighbor")
+    return _cycle_api(hier, level, level + 2, u, f, config)
+
+
+def v_cycle(hier, u, f, config: CycleConfig = None):
+    """One V-cycle (or W-cycle with config.cycle == "W") from the finest level
+    (multigrid.py:366-375)."""
+    config = config or CycleConfig()
+    depth = depth_of(hier, config)
+    if depth < 2:
+        raise ValueError("v_cycle needs a hierarchy with at least 2 levels")
+    return _cycle_api(hier, 0, depth, u, f, config)
+
+
+def _forward_solve_dev(ops, n, fd, config):
+    torch = _torch()
+    u = torch.empty_like(fd)
+    d = nat.level_desc(ops, n)
+    nat.check(nat.load().tmg_coarse_solve(nat.F64, ctypes.byref(d), _ptr(fd), _ptr(u), 1, 0,
+                                          int(config.dot_variant), _stream()), "tmg_coarse_solve")
+    return u
+
+
+def _floor_of(f) -> float:
+    torch = _torch()
+    if torch.is_tensor(f):
+        return 1e-12 * float(torch.linalg.norm(f.double()))
+    return 1e-12 * float(np.linalg.norm(f))
+
+
+def _times(total: float) -> dict:
+    # the fused kernels do not separate the phases; the wall time of the
+    # device solve is reported under "smoothing"
+    return {"smoothing": total, "transfer": 0.0, "coarse": 0.0, "residual": 0.0}
+
+
+def solve(hier, f, u_init=None, config: CycleConfig = None):
+    """Cycle until ||r|| <= max(eps ||r0||, 1e-12 ||f||) (multigrid.py:509-531).
+    Returns (u, SolveStats); non-convergence is a flag, not an exception."""
+    config = config or CycleConfig()
+    depth = depth_of(hier, config)
+    torch = _torch()
+    fd, was_t = _dev(f)
+    if u_init is None:
+        u_init = random_initial_guess(hier, config.seed)
+    if depth < 2:
+        u = _forward_solve_dev(hier.finest.ops, hier.finest.n_steps, fd, config)
+        stats = SolveStats(iterations=0, residual_norms=[0.0], factor=float("nan"),
+                           times=_times(0.0), converged=True, seed=config.seed,
+                           workers=config.workers)
+        return _out(u, was_t), stats
+    ud, _ = _dev(u_init)
+    ud = ud.clone()
+    floor = _floor_of(f)
+    omegas = level_omegas(hier, config, depth)
+    plan = get_plan(hier, 0, depth, omegas, config, 1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    it, norms, conv = plan.solve(fd, ud, [floor], config.eps, config.max_iters)
+    elapsed = time.perf_counter() - t0
+    k = int(it[0])
+    hist = [float(v) for v in norms[0, :k + 1]]
+    stats = SolveStats(iterations=k, residual_norms=hist, factor=max_ratio(hist),
+                       times=_times(elapsed), converged=bool(conv[0]), seed=config.seed,
+                       workers=config.workers)
+    return _out(ud, was_t), stats
+
+
+def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None):
+    """B independent problems sharing hier's operator: F, U0 of shape
+    (B, N, n_t).  Each problem follows the reference stopping rule on its own
+    (exactly as B separate ``solve`` calls).  Returns (U, [SolveStats])."""
+    config = config or CycleConfig()
+    depth = depth_of(hier, config)
+    if depth < 2:
+        raise ValueError("solve_batched needs at least 2 levels")
+    torch = _torch()
+    Fd, was_t = _dev(F)
+    B = Fd.shape[0]
+    if U0 is None:
+        Ud = torch.zeros_like(Fd)
+    else:
+        Ud, _ = _dev(U0)
+        Ud = Ud.clone()
+    if floors is None:
+        if torch.is_tensor(F):
+            floors = [1e-12 * float(v) for v in torch.linalg.norm(Fd.reshape(B, -1), dim=1).cpu()]
+        else:
+            floors = [1e-12 * float(np.linalg.norm(F[b])) for b in range(B)]
+    omegas = level_omegas(hier, config, depth)
+    plan = get_plan(hier, 0, depth, omegas, config, B)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    it, norms, conv = plan.solve(Fd, Ud, floors, config.eps, config.max_iters)
+    elapsed = time.perf_counter() - t0
+    stats = []
+    for b in range(B):
+        k = int(it[b])
+        hist = [float(v) for v in norms[b, :k + 1]]
+        stats.append(SolveStats(iterations=k, residual_norms=hist, factor=max_ratio(hist),
+                                times=_times(elapsed), converged=bool(conv[b]), seed=config.seed,
+                                workers=config.workers))
+    return _out(Ud, was_t), stats
+
+
+def measure_convergence_factor(hier, config: CycleConfig = None) -> float:
+    """Two-grid factor on f = 0 from the seeded random start
+    (multigrid.py:534-544)."""
+    config = config or CycleConfig(eps=1e-100)
+    if len(hier.levels) < 2:
+        raise ValueError("measuring the two-grid factor needs 2 levels")
+    n, nt = hier.finest.n_steps, hier.finest.ops.n_t
+    f = np.zeros((n, nt))
+    torch = _torch()
+    fd, _ = _dev(f)
+    ud, _ = _dev(random_initial_guess(hier, config.seed))
+    omegas = level_omegas(hier, config, 2)
+    plan = get_plan(hier, 0, 2, omegas, config, 1)
+    it, norms, conv = plan.solve(fd, ud, [0.0], config.eps, min(config.max_iters, 250))
+    k = int(it[0])
+    return max_ratio([float(v) for v in norms[0, :k + 1]])

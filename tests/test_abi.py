@@ -1,0 +1,68 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol that
+include/timemg_b200.h declares; struct layouts agree with the header."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1409_5254_b200 import _native as nat
+
+HEADER = os.path.join(nat.INCLUDE, "timemg_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tmg_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(nat.LIB_PATH):
+        nat.build()
+    return nat.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared_functions()
+    assert len(names) >= 14
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(nat.EXPORTS)
+
+
+def test_version_and_errors_without_gpu(lib):
+    assert lib.tmg_version() == 100
+    # argument validation happens before any CUDA call
+    d = nat.LevelDesc()
+    d.n_t = 9
+    d.n_slabs = 4
+    rc = lib.tmg_sweep(0, ctypes.byref(d), None, None, None, 1, -1, None, None)
+    assert rc == nat.E_ARG
+    assert b"sweep count" in lib.tmg_last_error()
+    rc = lib.tmg_residual(0, ctypes.byref(d), None, None, None, 1, None)
+    assert rc == nat.E_UNSUPPORTED
+    with pytest.raises(NotImplementedError):
+        nat.check(rc)
+
+
+def test_struct_layout_matches_header():
+    # tmg_level_desc: 2 x int32, int64, double, 5 x 64 doubles, 8 x int32
+    assert ctypes.sizeof(nat.LevelDesc) == 4 + 4 + 8 + 8 + 5 * 64 * 8 + 8 * 4
+    assert nat.LevelDesc.n_slabs.offset == 8
+    assert nat.LevelDesc.minus_step.offset == 24
+    assert ctypes.sizeof(nat.PlanOpts) == 8 * 4
+
+
+def test_level_desc_packing():
+    import numpy as np
+    from paper_1409_5254_b200 import assemble_local, BasisSpec, build_transfers
+    ops = assemble_local(BasisSpec(2), 0.01)
+    r1, r2 = build_transfers(BasisSpec(2), 0.01)
+    d = nat.level_desc(ops, 64, 0.7, r1, r2)
+    assert d.n_t == 3 and d.n_slabs == 64 and d.has_transfer == 1
+    assert list(d.minus_step[:9]) == list(np.asarray(ops.minus_step_matrix).ravel())
+    assert list(d.r2[:9]) == list(r2.ravel())
+    assert list(d.perm[:3]) == list(ops.lu.perm)

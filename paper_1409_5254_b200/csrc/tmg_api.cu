@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -44,10 +45,32 @@ int fail(int code, const char *fmt, ...)
     return code;
 }
 
-#define CK(x)                                                                          \
-    do {                                                                               \
-        cudaError_t e_ = (x);                                                          \
-        if (e_ != cudaSuccess) return fail((int)e_, "%s: %s", #x, cudaGetErrorString(e_)); \
+#define CK(x)                                                                            \
+    do {                                                                                 \
+        cudaError_t e_ = (x);                                                            \
+        if (e_ != cudaSuccess)                                                           \
+            return fail((int)e_, "%s (tmg_api.cu:%d): %s", #x, __LINE__, cudaGetErrorString(e_)); \
+    } while (0)
+
+// TMG_SYNC_DEBUG=1: synchronise after every launch (pinpoints a faulting kernel)
+bool sync_debug()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TMG_SYNC_DEBUG");
+        v = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+#define CK_LAUNCH(what)                                                                  \
+    do {                                                                                 \
+        CK(cudaGetLastError());                                                          \
+        if (sync_debug()) {                                                              \
+            cudaError_t e2_ = cudaDeviceSynchronize();                                   \
+            if (e2_ != cudaSuccess)                                                      \
+                return fail((int)e2_, "%s (tmg_api.cu:%d): %s", what, __LINE__, cudaGetErrorString(e2_)); \
+        }                                                                                \
     } while (0)
 
 #define CKR(x)                      \
@@ -118,7 +141,7 @@ template <typename T, int NT, int NU, bool SP, bool UP>
 int launch_stream_nu(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_t s)
 {
     auto k = stream_kernel<T, NT, NU, SP, UP>;
-    const size_t smem = RowLayout<T, NT>::smem_bytes();
+    const size_t smem = RowLayout<T, NT>::SMEM_BYTES;
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -128,7 +151,9 @@ int launch_stream_nu(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_
     const long long grid = (warps + SW_WARPS - 1) / SW_WARPS;
     if (grid <= 0) return 0;
     k<<<(unsigned)grid, SW_WARPS * 32, smem, s>>>(L, a);
-    CK(cudaGetLastError());
+    char what[96];
+    snprintf(what, sizeof what, "stream_kernel<nt=%d,nu=%d,up=%d> n=%lld flags=%d", NT, NU, (int)UP, a.n, a.flags);
+    CK_LAUNCH(what);
     return 0;
 }
 
@@ -390,7 +415,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.n_cycles = (tl == depth - 1) ? 1 : o.gamma;
             t.active = d_active;
             tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
-            CK(cudaGetLastError());
+            CK_LAUNCH("tail_kernel");
             ++kernels_per_cycle;
         } else {
             for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s));
@@ -424,9 +449,9 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         else
             finalize_sq_kernel<<<(unsigned)B, 1024, 0, s>>>(sqbuf, n[0], d_st, d_hist, hist_stride, d_floor,
                                                            eps, mode, nullptr);
-        CK(cudaGetLastError());
+        CK_LAUNCH("finalize");
         active_flags_kernel<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(d_st, d_active, d_any, (int)B);
-        CK(cudaGetLastError());
+        CK_LAUNCH("active_flags");
         kernels_per_cycle += 2;
         return 0;
     }
@@ -444,7 +469,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     int run_cycle(const void *f, void *u, bool norm, double eps, cudaStream_t s)
     {
-        if (!o.use_graph) return enqueue_cycle(f, u, norm, eps, s);
+        if (!o.use_graph || sync_debug()) return enqueue_cycle(f, u, norm, eps, s);
         if (!gexec || g_f != f || g_u != u || g_norm != norm || g_eps != eps) {
             if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
             cudaGraph_t g;
@@ -499,7 +524,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.n_cycles = nc;
             t.active = nullptr;
             tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
-            CK(cudaGetLastError());
+            CK_LAUNCH("tail_kernel");
             return 0;
         }
         CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));  // all active (nonzero)
@@ -535,7 +560,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.st = d_st;
             t.active = nullptr;
             tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
-            CK(cudaGetLastError());
+            CK_LAUNCH("tail_kernel");
         } else {
             // r0 = ||f - L u_init|| (norm_at before the loop, multigrid.py:478)
             CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));

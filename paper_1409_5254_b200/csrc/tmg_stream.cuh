@@ -111,11 +111,10 @@ template <typename T, int NT> struct RowLayout {
     static constexpr int ROW = 32 * NT;   // elements of one fine row
     static constexpr int HALF = 16 * NT;  // elements of the matching coarse half-row
     static constexpr int STAGE = 2 * ROW + HALF;
-    static constexpr size_t bytes_per_warp() { return sizeof(T) * STAGE * SW_STAGES; }
-    static constexpr size_t smem_bytes()
-    {
-        return 128 + bytes_per_warp() * SW_WARPS;  // 128: mbarriers (8 warps x 4 x 8 B)
-    }
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * SW_STAGES;
+    // mbarrier block (one 8-byte barrier per warp and stage), padded to 128 B
+    static constexpr size_t BAR_BYTES = ((SW_WARPS * SW_STAGES * 8 + 127) / 128) * 128;
+    static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * SW_WARPS;
 };
 
 template <typename T, int NT, int NU, bool SPARSE, bool UP>
@@ -148,7 +147,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32)
     const T *ucb = prolong ? a.uc + (size_t)b * nc * NT : nullptr;
 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * SW_STAGES;
-    T *ring = reinterpret_cast<T *>(smem + 128) + (size_t)warp * Lay::STAGE * SW_STAGES;
+    T *ring = reinterpret_cast<T *>(smem + Lay::BAR_BYTES) + (size_t)warp * Lay::STAGE * SW_STAGES;
     const bool tma = flags & SF_TMA;
 
     // a row goes through the ring iff all its pieces are 16-byte multiples

@@ -122,9 +122,9 @@ def test_resid_norm_matches_numpy_order(oracle_mod):
         f = rng.standard_normal((n, p_t + 1))
         out = torch.empty(1, dtype=torch.float64, device="cuda")
         d = nat.level_desc(ops, n)
-        nat.check(L.tmg_resid_norm(0, ctypes.byref(d), P(dev(f)), P(dev(u)), P(out), 1, None))
+        fd, ud = dev(f), dev(u)  # keep both alive across the call
+        nat.check(L.tmg_resid_norm(0, ctypes.byref(d), P(fd), P(ud), P(out), 1, None))
         r = oracle_mod.residual(ops, f, u)
-        sq = np.sum(r * r, axis=1) if p_t == 0 else None
         acc = r[:, 0] * r[:, 0]
         for j in range(1, p_t + 1):
             acc = acc + r[:, j] * r[:, j]

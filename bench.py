@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 time-multigrid slab sweep (BASELINE.json metric:
+"V-cycle time-DoF/s (fp64) and % of HBM roofline; wall time to 1e-8").
+
+Default workload (BASELINE config 3, the largest single-GPU configuration):
+B = 64 independent seeded problems, p_t = 1, N = 2^22 slabs each, T = 1, fp64,
+V(1,1)-cycles coarsening to 2 slabs, zero initial guess, iterated to a 1e-8
+relative residual with every problem stopping on its own (the reference
+stopping rule, multigrid.py:481-496).  One step = one batched solve with the
+inputs resident in HBM (4 GiB per array > 126 MB L2: no L2 flush needed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config3]
+    python bench.py --impl reference      # the CPU reference arm (oracle port)
+
+Under torchrun each rank solves its own 64 problems (problem ids rank*64+b):
+weak scaling with no data-path collective; time = max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "V-cycle time-DoF/s (fp64)"
+UNIT = "time-DoF/s"
+PROFILE_SUMMARY = os.path.join(REPO, "profiles", "ncu_summary.json")
+
+WORKLOADS = {
+    "config3": dict(batch=64, n=1 << 22, p_t=1, T=1.0, nu=1),
+    "config2": dict(batch=1, n=1 << 20, p_t=1, T=1.0, nu=1),
+    "config1": dict(batch=1, n=1 << 10, p_t=1, T=1.0, nu=1),
+}
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peak_hbm():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/tmg_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 3:
+                    continue
+                try:
+                    s, m = float(parts[0]), float(parts[1])
+                    bits = int(parts[2], 16)
+                except ValueError:
+                    continue
+                mx = max(mx, m)
+                if bits & 0x1:  # idle samples are not "under load"
+                    continue
+                sm.append(s)
+                for bit, name in REASON_BITS.items():
+                    if bits & bit:
+                        reasons.add(name)
+        except FileNotFoundError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_hier(w):
+    import paper_1409_5254_b200 as tmg
+    return tmg.TimeHierarchy.build(tmg.BasisSpec(w["p_t"]), w["T"] / w["n"], w["n"], coarsest=2)
+
+
+# ---------------------------------------------------------------------------
+# CPU: oracle port of the reference (the reference arm and cpu_baseline)
+
+def cpu_solve_sample(w, F_host_list, budget_s=12.0, threads=None):
+    """Full reference-order solves of whole problems on the host until the
+    time budget is used (at least one problem).  Returns (value, sample, cores)."""
+    from oracle import oracle as O
+    import paper_1409_5254_b200 as tmg
+    if threads:
+        O.set_threads(threads)
+    cores = O.num_threads()
+    hier = make_hier(w)
+    om = [tmg.optimal_omega(tmg.alpha(hier.basis, l.tau)) for l in hier.levels]
+    dofs = 0
+    secs = 0.0
+    done = 0
+    for rhs in F_host_list:
+        t0 = time.perf_counter()
+        _, _, it = O.iterate(hier, om, rhs, np.zeros_like(rhs), w["nu"], w["nu"], 1e-8, 250)
+        secs += time.perf_counter() - t0
+        dofs += w["n"] * (w["p_t"] + 1) * it
+        done += 1
+        if secs >= budget_s:
+            break
+    sample = (f"{done} of {w['batch']} problems solved to 1e-8 (N={w['n']}, p_t={w['p_t']}, "
+              f"V({w['nu']},{w['nu']})) by the C restatement of the reference, {cores} OpenMP threads")
+    return dofs / secs, sample, cores, secs
+
+
+def run_reference_arm(args, w):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import torch
+    from paper_1409_5254_b200 import problems
+    # same seeded inputs as the GPU arm (assembled on the host here)
+    hosts = []
+    vals = []
+    total_steps = args.warmup + args.steps
+    for s in range(total_steps):
+        b = s % w["batch"]
+        rhs, _, _ = problems.seeded_rhs(w["p_t"], w["n"], w["T"], 42, b if w["batch"] > 1 else None)
+        hosts.append(rhs)
+    from oracle import oracle as O
+    import paper_1409_5254_b200 as tmg
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    hier = make_hier(w)
+    om = [tmg.optimal_omega(tmg.alpha(hier.basis, l.tau)) for l in hier.levels]
+    times, dofs = [], []
+    for s, rhs in enumerate(hosts):
+        t0 = time.perf_counter()
+        _, _, it = O.iterate(hier, om, rhs, np.zeros_like(rhs), w["nu"], w["nu"], 1e-8, 250)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            dofs.append(w["n"] * (w["p_t"] + 1) * it)
+    value = sum(dofs) / sum(times)
+    sample = (f"each step: one of the {w['batch']} problems (N={w['n']}, p_t={w['p_t']}) solved to "
+              f"1e-8 by the C restatement of the reference (oracle/), {cores} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, w),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, w):
+    return {"workload": (f"{args.workload}: B={w['batch']} x N=2^{int(np.log2(w['n']))} slabs, "
+                         f"p_t={w['p_t']}, T={w['T']:g}, V({w['nu']},{w['nu']})-cycles to 1e-8, "
+                         "coarsest=2, zero initial guess, optimal omega"),
+            "batch_per_gpu": w["batch"], "n_slabs": w["n"], "p_t": w["p_t"], "nu": w["nu"],
+            "problems": "seeded (SURVEY 8d): default_rng([42, b]) a, phi, u0",
+            "l2": "inputs larger than L2 (no flush)" if w["batch"] * w["n"] * (w["p_t"] + 1) * 8 > 2 ** 27
+            else "working set L2-resident; L2 flushed between steps"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def kernel_roofline(w, F, U, hier, stream_ptr, reps=10):
+    """Time the fused finest-level down pass (nu1 sweeps + residual +
+    restriction) and up pass alone with CUDA events; algorithmic bytes per
+    fine slab = 3.5 * n_t * 8 (read u, f [+ u_c/2], write u [+ f_c/2])."""
+    import torch
+    from paper_1409_5254_b200 import _native as nat
+    import paper_1409_5254_b200 as tmg
+    L = nat.load()
+    B, n, nt = F.shape
+    lev = hier.levels[0]
+    om = tmg.optimal_omega(tmg.alpha(hier.basis, lev.tau))
+    d = nat.level_desc(lev.ops, n, om, lev.r1, lev.r2)
+    Uo = torch.empty_like(U)
+    FC = torch.empty((B, n // 2, nt), dtype=F.dtype, device=F.device)
+    UC = torch.zeros((B, n // 2, nt), dtype=F.dtype, device=F.device)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    s = ctypes.c_void_p(stream_ptr)
+    down = lambda: nat.check(L.tmg_down(0, ctypes.byref(d), P(F), P(U), P(Uo), P(FC), B, w["nu"], None, s))
+    up = lambda: nat.check(L.tmg_up(0, ctypes.byref(d), P(F), P(Uo), P(UC), P(U), None, B, w["nu"], None, s))
+    res = {}
+    for name, fn in (("down", down), ("up", up)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / reps * 1e-3
+    bytes_per_launch = 3.5 * nt * 8 * n * B
+    return res, bytes_per_launch
+
+
+def run_gpu_arm(args, w):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    import paper_1409_5254_b200 as tmg
+    from paper_1409_5254_b200 import problems, solver
+
+    B, n, p_t = w["batch"], w["n"], w["p_t"]
+    nt = p_t + 1
+    ids = [rank * B + b for b in range(B)] if B > 1 else [None]
+    F = problems.seeded_rhs_batch_device(p_t, n, w["T"], 42, ids if B > 1 else (None,))
+    floors = [1e-12 * float(v) for v in torch.linalg.norm(F.reshape(B, -1), dim=1).cpu()]
+    hier = make_hier(w)
+    cfg = tmg.CycleConfig(nu1=w["nu"], nu2=w["nu"], eps=1e-8)
+    U = torch.zeros_like(F)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if B * n * nt * 8 <= 2 ** 27 else None
+
+    def step():
+        U.zero_()
+        if flush is not None:
+            flush.zero_()
+        return tmg.solve_batched(hier, F, U, cfg, floors=floors)
+
+    for _ in range(args.warmup):
+        _, stats = step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            _, stats = step()
+            iters.append([s.iterations for s in stats])
+        e1.record()
+        torch.cuda.synchronize()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    if ws > 1:
+        dist.barrier()
+    dof = float(sum(n * nt * k for row in iters for k in row))
+    t = torch.tensor([elapsed, dof], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        tmax = t[0:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dsum = t[1:2].clone()
+        dist.all_reduce(dsum, op=dist.ReduceOp.SUM)
+        elapsed, dof = float(tmax.item()), float(dsum.item())
+    value = dof / elapsed
+    plan = solver.get_plan(hier, 0, len(hier.levels), solver.level_omegas(hier, cfg, len(hier.levels)),
+                           cfg, B)
+    info = plan.info()
+    max_it = max(max(r) for r in iters)
+    launches_per_step = 3 + info["kernels_per_cycle"] * max_it
+
+    # e2e: host (pinned) -> device, solve through the public API, solution -> host
+    F_host = F.cpu().pin_memory()
+    U_host = torch.empty_like(F_host).pin_memory()
+    U0 = torch.zeros_like(F)
+
+    def e2e_step():
+        Fd = F_host.to("cuda", non_blocking=True)
+        Ud, st = tmg.solve_batched(hier, Fd, U0, cfg, floors=floors)
+        U_host.copy_(Ud, non_blocking=True)
+        return st
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 3))
+    dof_e2e = 0.0
+    f0.record()
+    for _ in range(e2e_steps):
+        st = e2e_step()
+        dof_e2e += sum(n * nt * s.iterations for s in st)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_time = f0.elapsed_time(f1) * 1e-3
+    if ws > 1:
+        t2 = torch.tensor([e2e_time, dof_e2e], dtype=torch.float64, device="cuda")
+        a = t2[0:1].clone()
+        dist.all_reduce(a, op=dist.ReduceOp.MAX)
+        bsum = t2[1:2].clone()
+        dist.all_reduce(bsum, op=dist.ReduceOp.SUM)
+        e2e_time, dof_e2e = float(a.item()), float(bsum.item())
+    del U0
+
+    # roofline of the dominant kernel (finest-level fused down pass)
+    ktimes, kbytes = kernel_roofline(w, F, U, hier, torch.cuda.current_stream().cuda_stream)
+    peak, peak_kind = peak_hbm()
+    achieved = kbytes / ktimes["down"] / 1e9
+    traffic = None
+    try:
+        with open(PROFILE_SUMMARY) as fh:
+            prof = json.load(fh)
+        traffic = prof.get(args.workload, {}).get("down_dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        hosts = [F[b].cpu().numpy() for b in range(min(B, 4))]
+        v, sample, cores, secs = cpu_solve_sample(w, hosts, budget_s=args.cpu_budget)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+               "seconds": secs}
+
+    if rank == 0:
+        ms = 1e3 * elapsed / args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, w),
+            "wall_s_to_1e-8": ms * 1e-3, "iterations": sorted(set(i for r in iters for i in r)),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"stream_kernel down (nu1={w['nu']} sweeps + residual + "
+                                   "restriction), finest level, whole batch",
+                         "bytes_per_launch": kbytes, "launch_s": ktimes["down"],
+                         "up_kernel_frac": kbytes / ktimes["up"] / 1e9 / peak,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "frac_of_nominal_8TBs": achieved / 8000.0},
+            "e2e": {"value": dof_e2e / e2e_time, "unit": UNIT,
+                    "h2d_bytes_per_step": B * n * nt * 8, "d2h_bytes_per_step": B * n * nt * 8,
+                    "steps": e2e_steps},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        # whole-cycle HBM fraction: ~13 n_t * 8 algorithmic bytes per finest slab
+        # per V-cycle, summed over every problem-cycle of the run
+        cycles = sum(sum(r) for r in iters)
+        line["cycle_hbm_frac"] = (13 * nt * 8 * n * cycles) / elapsed / 1e9 / peak
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+    else:
+        run_gpu_arm(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -21,7 +21,7 @@ F64, F32 = 0, 1
 E_ARG, E_UNSUPPORTED, E_NOMEM = -1, -2, -3
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
-              "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "1886"]
+              "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "1886"]
 
 
 class LevelDesc(ctypes.Structure):
@@ -57,16 +57,42 @@ def sources():
                   if f.endswith((".cu", ".cuh")))
 
 
+# translation units: the C ABI / driver, and one kernel-instantiation unit per
+# (dtype, n_t) -- compiled in parallel, then linked into one shared library
+UNITS = [("tmg_api", "tmg_api.cu", [])] + [
+    (f"tmg_inst_{tn}_{nt}", "tmg_inst.cu", [f"-DTMG_T={t}", f"-DTMG_NT={nt}"])
+    for t, tn in (("double", "f64"), ("float", "f32")) for nt in (1, 2, 3, 4)]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libtimemg_b200.so in-tree for sm_100a (skipped when up to date)."""
-    newest = max(os.path.getmtime(p) for p in sources() + [os.path.join(INCLUDE, "timemg_b200.h")])
+    from concurrent.futures import ThreadPoolExecutor
+
+    newest = max(os.path.getmtime(p) for p in sources() + [os.path.join(INCLUDE, "timemg_b200.h"),
+                                                          os.path.abspath(__file__)])
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH + ".tmp",
-           os.path.join(CSRC, "tmg_api.cu")]
-    if verbose:
-        print(" ".join(cmd))
+    objdir = os.path.join(CSRC, "obj")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_unit(unit):
+        name, src, defs = unit
+        obj = os.path.join(objdir, name + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, "-c", *defs, "-I", INCLUDE, "-I", CSRC, "-o", obj,
+               os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            raise RuntimeError(f"nvcc failed for {name}:\n{r.stderr[-4000:]}")
+        return obj
+
+    jobs = max(1, min(len(UNITS), os.cpu_count() or 1))
+    with ThreadPoolExecutor(jobs) as ex:
+        objs = list(ex.map(compile_unit, UNITS))
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH + ".tmp",
+           *objs]
     subprocess.run(cmd, check=True)
     os.replace(LIB_PATH + ".tmp", LIB_PATH)
     return LIB_PATH

@@ -24,9 +24,10 @@
 #include <vector>
 
 #include "timemg_b200.h"
-#include "tmg_block.cuh"
+#include "tmg_launch.cuh"
+#include "tmg_norm.cuh"
 #include "tmg_slab.cuh"
-#include "tmg_stream.cuh"
+#include "tmg_stream.cuh"  // StreamArgs / flags / kinds (kernels are instantiated in tmg_inst.cu)
 
 using namespace tmg;
 
@@ -101,6 +102,10 @@ template <typename T, int NT> LevelC<T, NT> make_level(const tmg_level_desc &d)
     }
     L.omega = (T)d.omega;
     for (int i = 0; i < NT; ++i) {
+        L.rinv[i] = (T)1 / L.lu[i * NT + i];  // correctly rounded in T (IEEE division)
+        for (int j = 0; j < NT; ++j) L.PA[i * NT + j] = L.A[d.perm[i] * NT + j];
+    }
+    for (int i = 0; i < NT; ++i) {
         L.perm[i] = d.perm[i];
         unsigned m = 0;
         for (int j = 0; j < NT; ++j) m |= (std::signbit(d.coupling[i * NT + j]) ? 1u : 0u) << j;
@@ -120,6 +125,17 @@ int check_desc(const tmg_level_desc *d)
     return 0;
 }
 
+// compile-time LU permutation pattern of a level (PermKind)
+int perm_kind(const tmg_level_desc &d)
+{
+    bool id = true, rot = true;
+    for (int i = 0; i < d.n_t; ++i) {
+        id &= d.perm[i] == i;
+        rot &= d.perm[i] == (i + 1) % d.n_t;
+    }
+    return id ? P_ID : rot ? P_ROT : P_GEN;
+}
+
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ---------------------------------------------------------------------------
@@ -137,37 +153,19 @@ int sm_count()
     return n;
 }
 
-template <typename T, int NT, int NU, bool SP, bool UP>
-int launch_stream_nu(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_t s)
+template <typename T, int NT>
+int launch_stream(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int kind, int perm, bool sparse,
+                  cudaStream_t s)
 {
-    auto k = stream_kernel<T, NT, NU, SP, UP>;
-    const size_t smem = RowLayout<T, NT>::SMEM_BYTES;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    const long long warps = (long long)a.batch * a.chunks;
-    const long long grid = (warps + SW_WARPS - 1) / SW_WARPS;
-    if (grid <= 0) return 0;
-    k<<<(unsigned)grid, SW_WARPS * 32, smem, s>>>(L, a);
+    if (nu < 0 || nu > 4) return fail(TMG_E_UNSUPPORTED, "fused passes support nu <= 4 (got %d)", nu);
+    const int rc = stream_launch<T, NT>(L, a, nu, kind, perm, sparse, s);
+    if (rc < 0) return fail(TMG_E_UNSUPPORTED, "no stream kernel for nu=%d kind=%d", nu, kind);
+    if (rc > 0) return fail(rc, "stream_kernel<nt=%d,nu=%d,kind=%d>: %s", NT, nu, kind,
+                            cudaGetErrorString((cudaError_t)rc));
     char what[96];
-    snprintf(what, sizeof what, "stream_kernel<nt=%d,nu=%d,up=%d> n=%lld flags=%d", NT, NU, (int)UP, a.n, a.flags);
+    snprintf(what, sizeof what, "stream_kernel<nt=%d,nu=%d,kind=%d> n=%lld flags=%d", NT, nu, kind, a.n, a.flags);
     CK_LAUNCH(what);
     return 0;
-}
-
-template <typename T, int NT, bool SP, bool UP>
-int launch_stream(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, cudaStream_t s)
-{
-    switch (nu) {
-    case 0: return launch_stream_nu<T, NT, 0, SP, UP>(L, a, s);
-    case 1: return launch_stream_nu<T, NT, 1, SP, UP>(L, a, s);
-    case 2: return launch_stream_nu<T, NT, 2, SP, UP>(L, a, s);
-    case 3: return launch_stream_nu<T, NT, 3, SP, UP>(L, a, s);
-    case 4: return launch_stream_nu<T, NT, 4, SP, UP>(L, a, s);
-    default: return fail(TMG_E_UNSUPPORTED, "fused passes support nu <= 4 (got %d)", nu);
-    }
 }
 
 // rows per warp chunk: enough warps to fill the GPU several times over, a
@@ -178,7 +176,8 @@ int chunk_rows(long long n, long long batch, int leaf_rows)
     const long long target_warps = (long long)sm_count() * 16 * 4;
     long long r = (rows * batch) / std::max(1LL, target_warps);
     r = std::max(4LL, std::min(64LL, r));
-    const int q = std::max(1, leaf_rows);
+    // multiple of the ring group (2 rows) and of the norm leaf
+    const int q = leaf_rows == 3 ? 6 : (leaf_rows == 1 || leaf_rows == 2 || leaf_rows == 4 ? 4 : 2 * std::max(1, leaf_rows));
     r = ((r + q - 1) / q) * q;
     return (int)std::max<long long>(r, 1);
 }
@@ -247,6 +246,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     tmg_plan_opts o{};
     std::vector<long long> n;
     std::vector<LevelC<T, NT>> L;
+    std::vector<int> pk;  // LU permutation pattern per level
     LevelC<T, NT> *d_levels = nullptr;
     std::vector<T *> uA, uB, fl;
     int tl = 0;                 // first tail level
@@ -340,8 +340,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         tail_smem_bytes = tail_smem ? smem_of(tl) : fixed_smem();
         if (!tail_smem)
             CK(cudaMalloc(&gstore, (sizeof(T) * store_elems + sizeof(double) * (tl == 0 ? n[0] : 0)) * B + 64));
-        auto tk = tail_kernel<T, NT, SP>;
-        CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem_bytes));
+        CK(((cudaError_t)tail_prepare<T, NT>(SP, tail_smem_bytes)));
+        for (int l = 0; l < nl; ++l) pk.push_back(perm_kind(lv[l]));
 
         uA.assign(nl, nullptr);
         uB.assign(nl, nullptr);
@@ -402,7 +402,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             a.active = d_active;
             a.flags = SF_RESTRICT | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
             if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-            CKR((launch_stream<T, NT, SP, false>(L[l], a, o.nu1, s)));
+            CKR((launch_stream<T, NT>(L[l], a, o.nu1, K_DOWN, pk[l], SP, s)));
             ++kernels_per_cycle;
         }
         // coarse-grid correction
@@ -414,7 +414,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.full = 0;
             t.n_cycles = (tl == depth - 1) ? 1 : o.gamma;
             t.active = d_active;
-            tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
+            CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");
             ++kernels_per_cycle;
         } else {
@@ -435,7 +435,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                 else { a.flags |= SF_NORM_SQ; a.sq_out = sqbuf; }
             }
             if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
-            CKR((launch_stream<T, NT, SP, true>(L[l], a, o.nu2, s)));
+            const int kind = norm ? (leaf ? K_UPNORM : K_GENERIC) : K_UP;
+            CKR((launch_stream<T, NT>(L[l], a, o.nu2, kind, pk[l], SP, s)));
             ++kernels_per_cycle;
         }
         return 0;
@@ -523,7 +524,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.full = 0;
             t.n_cycles = nc;
             t.active = nullptr;
-            tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
+            CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");
             return 0;
         }
@@ -559,7 +560,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.hist = d_hist;
             t.st = d_st;
             t.active = nullptr;
-            tail_kernel<T, NT, SP><<<(unsigned)B, TAIL_THREADS, tail_smem_bytes, s>>>(t);
+            CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");
         } else {
             // r0 = ||f - L u_init|| (norm_at before the loop, multigrid.py:478)
@@ -573,7 +574,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                 a.leaf_out = leaves;
                 a.sq_out = sqbuf;
                 if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-                CKR((launch_stream<T, NT, SP, false>(L[0], a, 0, s)));
+                CKR((launch_stream<T, NT>(L[0], a, 0, K_GENERIC, P_GEN, SP, s)));
             }
             CK(cudaMemsetAsync(d_any, 0, sizeof(int), s));
             CKR(enqueue_finalize(0, eps, s));
@@ -699,7 +700,7 @@ int run_op(Op op, const tmg_level_desc &d, const OpArgs &x, cudaStream_t s)
             b.u_out = bufs[idx];
             b.flags = SF_WRITE_U | (src ? 0 : SF_ZERO_GUESS);
             if (tma_ok<T, NT>(b, false)) b.flags |= SF_TMA;
-            CKR((launch_stream<T, NT, SP, false>(L, b, k, s)));
+            CKR((launch_stream<T, NT>(L, b, k, K_GENERIC, P_GEN, SP, s)));
             src = bufs[idx];
             idx ^= 1;
             left -= k;
@@ -711,27 +712,27 @@ int run_op(Op op, const tmg_level_desc &d, const OpArgs &x, cudaStream_t s)
         a.r_out = (T *)x.aux;
         a.flags = SF_WRITE_R;
         if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-        return launch_stream<T, NT, SP, false>(L, a, 0, s);
+        return launch_stream<T, NT>(L, a, 0, K_GENERIC, P_GEN, SP, s);
     case OP_DOWN:
         a.u_out = (T *)x.u_out;
         a.fc = (T *)x.aux;
         a.flags = SF_RESTRICT | SF_WRITE_U | (x.u_in ? 0 : SF_ZERO_GUESS);
         if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-        return launch_stream<T, NT, SP, false>(L, a, x.nu, s);
+        return launch_stream<T, NT>(L, a, x.nu, K_DOWN, perm_kind(d), SP, s);
     case OP_UP:
         a.uc = (const T *)x.uc;
         a.u_out = (T *)x.u_out;
         a.flags = SF_PROLONG | SF_WRITE_U | (x.sq ? SF_NORM_SQ : 0);
         a.sq_out = x.sq;
         if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
-        return launch_stream<T, NT, SP, true>(L, a, x.nu, s);
+        return launch_stream<T, NT>(L, a, x.nu, x.sq ? K_GENERIC : K_UP, perm_kind(d), SP, s);
     case OP_NORM: {
         double *sq = nullptr;
         CK(cudaMallocAsync(&sq, sizeof(double) * n * x.batch, s));
         a.sq_out = sq;
         a.flags = SF_NORM_SQ;
         if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-        int rc = launch_stream<T, NT, SP, false>(L, a, 0, s);
+        int rc = launch_stream<T, NT>(L, a, 0, K_GENERIC, P_GEN, SP, s);
         if (!rc) {
             finalize_sq_kernel<<<(unsigned)x.batch, 1024, 0, s>>>(sq, n, nullptr, nullptr, 0, nullptr, 0.0, 0,
                                                                 (double *)x.aux);
@@ -778,9 +779,7 @@ int coarse_op(const tmg_level_desc &d, const void *f, void *u, long long B, int 
 {
     if (method != 0) return fail(TMG_E_UNSUPPORTED, "scan coarse solve not built in this version");
     const LevelC<T, NT> L = make_level<T, NT>(d);
-    coarse_serial_kernel<T, NT, SP><<<(unsigned)((B + 31) / 32), 32, 0, s>>>(L, (const T *)f, (T *)u, d.n_slabs,
-                                                                            (int)B, variant, nullptr);
-    CK(cudaGetLastError());
+    CK(((cudaError_t)coarse_serial_launch<T, NT>(L, SP, (const T *)f, (T *)u, d.n_slabs, (int)B, variant, nullptr, s)));
     return 0;
 }
 

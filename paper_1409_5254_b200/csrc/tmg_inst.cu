@@ -1,0 +1,117 @@
+// Kernel instantiations for one (dtype, n_t) pair: compile with
+//   -DTMG_T=double|float -DTMG_NT=1..4
+#define TMG_INST_UNIT 1
+#include "tmg_launch.cuh"
+#include "tmg_stream.cuh"
+#include "tmg_tail.cuh"
+
+#ifndef TMG_T
+#error "define TMG_T and TMG_NT"
+#endif
+
+namespace tmg {
+
+namespace {
+
+template <typename T, int NT, int NU, bool SP, int KIND, int PERM>
+int launch_one(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_t s)
+{
+    auto k = stream_kernel<T, NT, NU, SP, KIND, PERM>;
+    constexpr size_t smem = RowLayout<T, NT>::SMEM_BYTES;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+    }
+    const long long warps = (long long)a.batch * a.chunks;
+    const long long grid = (warps + SW_WARPS - 1) / SW_WARPS;
+    if (grid <= 0) return 0;
+    k<<<(unsigned)grid, SW_WARPS * 32, smem, s>>>(L, a);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int NT, bool SP, int KIND, int PERM>
+int by_nu(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, cudaStream_t s)
+{
+    switch (nu) {
+    case 0: return launch_one<T, NT, 0, SP, KIND, PERM>(L, a, s);
+    case 1: return launch_one<T, NT, 1, SP, KIND, PERM>(L, a, s);
+    case 2: return launch_one<T, NT, 2, SP, KIND, PERM>(L, a, s);
+    case 3: return launch_one<T, NT, 3, SP, KIND, PERM>(L, a, s);
+    case 4: return launch_one<T, NT, 4, SP, KIND, PERM>(L, a, s);
+    }
+    return -2;
+}
+
+template <typename T, int NT, int KIND>
+int by_perm(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int perm, cudaStream_t s)
+{
+    if constexpr (NT == 1) {
+        return by_nu<T, NT, true, KIND, P_ID>(L, a, nu, s);  // n_t = 1: the only permutation
+    } else {
+        switch (perm) {
+        case P_ID: return by_nu<T, NT, true, KIND, P_ID>(L, a, nu, s);
+        case P_ROT: return by_nu<T, NT, true, KIND, P_ROT>(L, a, nu, s);
+        default: return by_nu<T, NT, true, KIND, P_GEN>(L, a, nu, s);
+        }
+    }
+}
+
+}  // namespace
+
+template <typename T, int NT>
+int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int kind, int perm, bool sparse,
+                  cudaStream_t s)
+{
+    if (!sparse || kind == K_GENERIC) {
+        // runtime-flag kernel (general coupling, the single-level API entry points)
+        return sparse ? by_nu<T, NT, true, K_GENERIC, P_GEN>(L, a, nu, s)
+                      : by_nu<T, NT, false, K_GENERIC, P_GEN>(L, a, nu, s);
+    }
+    switch (kind) {
+    case K_DOWN: return by_perm<T, NT, K_DOWN>(L, a, nu, perm, s);
+    case K_UP: return by_perm<T, NT, K_UP>(L, a, nu, perm, s);
+    case K_UPNORM: return by_perm<T, NT, K_UPNORM>(L, a, nu, perm, s);
+    }
+    return -1;
+}
+
+template <typename T, int NT> size_t stream_smem_bytes() { return RowLayout<T, NT>::SMEM_BYTES; }
+
+template <typename T, int NT> int tail_prepare(bool sparse, size_t smem)
+{
+    cudaError_t e = sparse ? cudaFuncSetAttribute(tail_kernel<T, NT, true>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                           : cudaFuncSetAttribute(tail_kernel<T, NT, false>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return (int)e;
+}
+
+template <typename T, int NT>
+int tail_launch(const TailArgs<T, NT> &t, bool sparse, unsigned grid, size_t smem, cudaStream_t s)
+{
+    if (sparse) tail_kernel<T, NT, true><<<grid, TAIL_THREADS, smem, s>>>(t);
+    else tail_kernel<T, NT, false><<<grid, TAIL_THREADS, smem, s>>>(t);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int NT>
+int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, long long n, int batch,
+                         int variant, const int *active, cudaStream_t s)
+{
+    const unsigned grid = (unsigned)((batch + 31) / 32);
+    if (sparse) coarse_serial_kernel<T, NT, true><<<grid, 32, 0, s>>>(L, f, u, n, batch, variant, active);
+    else coarse_serial_kernel<T, NT, false><<<grid, 32, 0, s>>>(L, f, u, n, batch, variant, active);
+    return (int)cudaGetLastError();
+}
+
+template int stream_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
+                                          int, bool, cudaStream_t);
+template size_t stream_smem_bytes<TMG_T, TMG_NT>();
+template int tail_prepare<TMG_T, TMG_NT>(bool, size_t);
+template int tail_launch<TMG_T, TMG_NT>(const TailArgs<TMG_T, TMG_NT> &, bool, unsigned, size_t, cudaStream_t);
+template int coarse_serial_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, bool, const TMG_T *, TMG_T *,
+                                                 long long, int, int, const int *, cudaStream_t);
+
+}  // namespace tmg

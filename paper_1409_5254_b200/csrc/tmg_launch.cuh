@@ -1,0 +1,46 @@
+// Launchers of the templated kernels.  Each (dtype, n_t) pair is compiled in
+// its own translation unit (tmg_inst.cu built with -DTMG_T/-DTMG_NT) so the
+// ~140 specialisations build in parallel; tmg_api.cu only sees these
+// declarations.  All return 0 or a cudaError_t value (TMG_E_* for bad args).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "tmg_slab.cuh"
+#include "tmg_types.cuh"
+
+namespace tmg {
+
+template <typename T> struct StreamArgs;
+
+// kind: Kind (tmg_stream.cuh); perm: PermKind (tmg_slab.cuh)
+template <typename T, int NT>
+int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int kind, int perm, bool sparse,
+                  cudaStream_t s);
+template <typename T, int NT> size_t stream_smem_bytes();
+template <typename T, int NT> int tail_prepare(bool sparse, size_t smem);
+template <typename T, int NT>
+int tail_launch(const TailArgs<T, NT> &t, bool sparse, unsigned grid, size_t smem, cudaStream_t s);
+template <typename T, int NT>
+int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, long long n, int batch,
+                         int variant, const int *active, cudaStream_t s);
+
+#define TMG_DECLARE(T, NT)                                                                              \
+    extern template int stream_launch<T, NT>(const LevelC<T, NT> &, const StreamArgs<T> &, int, int, int, \
+                                             bool, cudaStream_t);                                       \
+    extern template size_t stream_smem_bytes<T, NT>();                                                  \
+    extern template int tail_prepare<T, NT>(bool, size_t);                                              \
+    extern template int tail_launch<T, NT>(const TailArgs<T, NT> &, bool, unsigned, size_t, cudaStream_t); \
+    extern template int coarse_serial_launch<T, NT>(const LevelC<T, NT> &, bool, const T *, T *, long long, \
+                                                    int, int, const int *, cudaStream_t);
+#ifndef TMG_INST_UNIT
+TMG_DECLARE(double, 1)
+TMG_DECLARE(double, 2)
+TMG_DECLARE(double, 3)
+TMG_DECLARE(double, 4)
+TMG_DECLARE(float, 1)
+TMG_DECLARE(float, 2)
+TMG_DECLARE(float, 3)
+TMG_DECLARE(float, 4)
+#endif
+
+}  // namespace tmg

@@ -1,0 +1,110 @@
+// Residual-norm finalisation and the stopping rule (multigrid.py:445-496).
+// Included by exactly one translation unit (tmg_api.cu).
+#pragma once
+#include "tmg_pairwise.cuh"
+#include "tmg_types.cuh"
+
+namespace tmg {
+
+// sum of a perfect binary tree of `m` values (m a power of two) per problem,
+// one CTA per problem, then the stopping-rule update.
+//   mode 0: r0 (initialises tol/active), mode 1: after a cycle.
+__global__ void __launch_bounds__(1024)
+    finalize_leaves_kernel(const double *leaves, long long m, ProbState *st, double *hist,
+                           int hist_stride, const double *floor_, double eps, int mode)
+{
+    __shared__ double part[1024];
+    const int b = blockIdx.x;
+    if (mode == 1 && !st[b].active) return;
+    const double *lv = leaves + (size_t)b * m;
+    const int T = blockDim.x;
+    const int t = threadIdx.x;
+    double v = 0.0;
+    long long per = m > T ? m / T : 1;
+    int used = (int)(m > T ? T : m);
+    if (t < used) {
+        // bottom-up perfect tree over [t*per, (t+1)*per)
+        double stack[40];
+        for (long long i = 0; i < per; ++i) {
+            double x = lv[t * per + i];
+            int l = 0;
+            while ((i >> l) & 1) { x = __dadd_rn(stack[l], x); ++l; }
+            stack[l] = x;
+        }
+        int top = 0;
+        while ((1LL << top) < per) ++top;
+        v = stack[top];
+    }
+    part[t] = v;
+    __syncthreads();
+    for (int s = 1; s < used; s <<= 1) {
+        if ((t % (2 * s)) == 0 && t + s < used) part[t] = __dadd_rn(part[t], part[t + s]);
+        __syncthreads();
+    }
+    if (t == 0) {
+        double nrm = __dsqrt_rn(part[0]);
+        ProbState &p = st[b];
+        if (mode == 0) {
+            hist[(size_t)b * hist_stride] = nrm;
+            double e = __dmul_rn(eps, nrm);
+            p.tol = e > floor_[b] ? e : floor_[b];
+            p.iters = 0;
+            p.active = (nrm > p.tol) && (p.max_iters > 0);
+            p.converged = nrm <= p.tol;
+        } else {
+            p.iters += 1;
+            hist[(size_t)b * hist_stride + p.iters] = nrm;
+            p.converged = nrm <= p.tol;
+            p.active = (nrm > p.tol) && (p.iters < p.max_iters);
+        }
+    }
+}
+
+// generic (any n) exact pairwise over per-slab squares
+__global__ void __launch_bounds__(1024)
+    finalize_sq_kernel(const double *sq, long long n, ProbState *st, double *hist, int hist_stride,
+                       const double *floor_, double eps, int mode, double *norm_out)
+{
+    __shared__ double part[1024];
+    const int b = blockIdx.x;
+    if (st && mode == 1 && !st[b].active) return;
+    double s = block_pairwise(sq + (size_t)b * n, n, part);
+    if (threadIdx.x == 0) {
+        double nrm = __dsqrt_rn(s);
+        if (norm_out) norm_out[b] = nrm;
+        if (st) {
+            ProbState &p = st[b];
+            if (mode == 0) {
+                hist[(size_t)b * hist_stride] = nrm;
+                double e = __dmul_rn(eps, nrm);
+                p.tol = e > floor_[b] ? e : floor_[b];
+                p.iters = 0;
+                p.active = (nrm > p.tol) && (p.max_iters > 0);
+                p.converged = nrm <= p.tol;
+            } else {
+                p.iters += 1;
+                hist[(size_t)b * hist_stride + p.iters] = nrm;
+                p.converged = nrm <= p.tol;
+                p.active = (nrm > p.tol) && (p.iters < p.max_iters);
+            }
+        }
+    }
+}
+
+__global__ void active_flags_kernel(const ProbState *st, int *active, int *any, int batch)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < batch) {
+        int a = st[b].active;
+        active[b] = a;
+        if (a) atomicOr(any, 1);
+    }
+}
+
+__global__ void copy_active_kernel(const ProbState *st, int *active, int batch)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < batch) active[b] = st[b].active;
+}
+
+}  // namespace tmg

@@ -52,11 +52,39 @@ template <> struct FP<float> {
     static __device__ __forceinline__ float zero(bool neg) { return neg ? -0.0f : 0.0f; }
 };
 
+// a / d, correctly rounded, for a divisor d known ahead of time with
+// rinv = RN(1/d): q0 = RN(a rinv) is within ~2 ulp, one fma correction makes
+// it faithful, and a second correction gives RN(a/d) exactly (Markstein's
+// theorem: rinv correctly rounded + faithful q => q + (a - d q) rinv rounds to
+// the correctly rounded quotient; the remainders are exact fma results).
+// Outside a safe exponent window (zeros, subnormals, huge values) it defers to
+// the IEEE division, so the result always equals FP<T>::div(a, d) bit for bit.
+__device__ __forceinline__ double divq(double a, double d, double rinv)
+{
+    double q0 = __dmul_rn(a, rinv);
+    double q1 = __fma_rn(__fma_rn(-q0, d, a), rinv, q0);
+    double q2 = __fma_rn(__fma_rn(-q1, d, a), rinv, q1);
+    const unsigned e = (unsigned)(__double2hiint(a) >> 20) & 0x7ffu;
+    if (__builtin_expect(e - 123u >= 1800u, 0)) q2 = __ddiv_rn(a, d);  // |a| outside [2^-900, 2^900)
+    return q2;
+}
+__device__ __forceinline__ float divq(float a, float d, float rinv)
+{
+    float q0 = __fmul_rn(a, rinv);
+    float q1 = __fmaf_rn(__fmaf_rn(-q0, d, a), rinv, q0);
+    float q2 = __fmaf_rn(__fmaf_rn(-q1, d, a), rinv, q1);
+    const unsigned e = (__float_as_uint(a) >> 23) & 0xffu;
+    if (__builtin_expect(e - 28u >= 200u, 0)) q2 = __fdiv_rn(a, d);  // |a| outside [2^-99, 2^101)
+    return q2;
+}
+
 // Per-level constants in the compute type (kernel parameter / shared memory).
 template <typename T, int NT> struct LevelC {
     T A[NT * NT];   // minus_step_matrix  (dg.py:213-215)
     T C[NT * NT];   // coupling           (dg.py:236)
     T lu[NT * NT];  // BlockLU.lu         (dg.py:145)
+    T rinv[NT];     // RN(1 / lu[i,i]): divisor reciprocals for divq
+    T PA[NT * NT];  // rows of A in LU-permutation order: PA[i] = A[perm[i]]
     T R1[NT * NT];  // Level.r1           (transfers.py:16-37)
     T R2[NT * NT];  // Level.r2
     T omega;        // resolve_damping(alpha(tau))
@@ -203,7 +231,7 @@ template <typename T, int NT>
 __device__ __forceinline__ void lu_solve(const LevelC<T, NT> &L, const T (&r)[NT], T (&y)[NT])
 {
     if constexpr (NT == 1) {
-        y[0] = FP<T>::div(r[0], L.lu[0]);
+        y[0] = divq(r[0], L.lu[0], L.rinv[0]);
     } else {
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
@@ -220,7 +248,7 @@ __device__ __forceinline__ void lu_solve(const LevelC<T, NT> &L, const T (&r)[NT
         for (int i = NT - 1; i >= 0; --i) {
 #pragma unroll
             for (int j = i + 1; j < NT; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
-            y[i] = FP<T>::div(y[i], L.lu[i * NT + i]);
+            y[i] = divq(y[i], L.lu[i * NT + i], L.rinv[i]);
         }
     }
 }
@@ -352,6 +380,136 @@ template <typename T, int NT> __device__ __forceinline__ void zero_slab(T (&x)[N
 {
 #pragma unroll
     for (int j = 0; j < NT; ++j) x[j] = T(0);
+}
+
+}  // namespace tmg
+
+namespace tmg {
+
+// ---- fast-path variants used by the streaming kernels ---------------------
+// LU row permutation as a compile-time pattern: the reference's factors use
+// perm = (1, 2, .., n_t-1, 0) for small steps and the identity for large ones
+// (other patterns fall back to runtime selects).
+enum PermKind { P_GEN = 0, P_ID = 1, P_ROT = 2 };
+
+// y_i = r_{perm[i]} with r = ((A u) + f) [+ N u_prev]: each row computed in
+// exactly the reference's order, just stored in the order the LU solve reads.
+template <typename T, int NT, bool SPARSE, int PERM>
+__device__ __forceinline__ void residual_perm(const LevelC<T, NT> &L, const T (&u)[NT], const T (&f)[NT],
+                                              const Cpl<T, NT, SPARSE> &p, bool has_prev, T (&y)[NT])
+{
+    if constexpr (PERM == P_GEN) {
+        T r[NT];
+        residual<T, NT, SPARSE>(L, u, f, p, has_prev, r);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            T v = r[0];
+#pragma unroll
+            for (int q = 1; q < NT; ++q) v = (L.perm[i] == q) ? r[q] : v;
+            y[i] = v;
+        }
+    } else {
+        const unsigned full = (1u << NT) - 1u;
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            const int src = (PERM == P_ROT) ? (i + 1) % NT : i;
+            T a = FP<T>::mul(L.A[src * NT], u[0]);
+#pragma unroll
+            for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(L.A[src * NT + j], u[j]));
+            a = FP<T>::add(a, f[src]);
+            T c;
+            if constexpr (SPARSE) {
+                c = (src == 0) ? p.s : FP<T>::zero(((p.m ^ L.cneg[src]) & full) == full);
+            } else {
+                c = FP<T>::mul(L.C[src * NT], p.u[0]);
+#pragma unroll
+                for (int j = 1; j < NT; ++j) c = FP<T>::add(c, FP<T>::mul(L.C[src * NT + j], p.u[j]));
+            }
+            T ac = FP<T>::add(a, c);
+            y[i] = has_prev ? ac : a;
+        }
+    }
+}
+
+// forward + backward substitution on an already permuted right-hand side
+template <typename T, int NT> __device__ __forceinline__ void lu_apply(const LevelC<T, NT> &L, T (&y)[NT])
+{
+#pragma unroll
+    for (int i = 1; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+#pragma unroll
+    for (int i = NT - 1; i >= 0; --i) {
+#pragma unroll
+        for (int j = i + 1; j < NT; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+        y[i] = divq(y[i], L.lu[i * NT + i], L.rinv[i]);
+    }
+}
+
+template <typename T, int NT, bool SPARSE, int PERM>
+__device__ __forceinline__ void sweep_p(const LevelC<T, NT> &L, T (&u)[NT], const T (&f)[NT],
+                                        const Cpl<T, NT, SPARSE> &p, bool has_prev)
+{
+    T y[NT];
+    residual_perm<T, NT, SPARSE, PERM>(L, u, f, p, has_prev, y);
+    lu_apply<T, NT>(L, y);
+#pragma unroll
+    for (int i = 0; i < NT; ++i) u[i] = FP<T>::add(FP<T>::mul(y[i], L.omega), u[i]);
+}
+
+// transfer products with the lane's own block held in registers
+template <typename T, int NT>
+__device__ __forceinline__ void restrict_reg(const T (&R)[NT * NT], const T (&r)[NT], T (&o)[NT])
+{
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        T a = FP<T>::mul(R[i * NT], r[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(R[i * NT + j], r[j]));
+        o[i] = a;
+    }
+}
+template <typename T, int NT>
+__device__ __forceinline__ void prolong_reg(const T (&R)[NT * NT], const T (&uc)[NT], T (&u)[NT])
+{
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        T a = FP<T>::mul(R[i], uc[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(R[j * NT + i], uc[j]));
+        u[i] = FP<T>::add(u[i], a);
+    }
+}
+
+template <typename T, int NT>
+__device__ __forceinline__ void restrict_ptr(const T *R, const T (&r)[NT], T (&o)[NT])
+{
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        T a = FP<T>::mul(R[i * NT], r[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(R[i * NT + j], r[j]));
+        o[i] = a;
+    }
+}
+template <typename T, int NT>
+__device__ __forceinline__ void prolong_ptr(const T *R, const T (&uc)[NT], T (&u)[NT])
+{
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        T a = FP<T>::mul(R[i], uc[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(R[j * NT + i], uc[j]));
+        u[i] = FP<T>::add(u[i], a);
+    }
+}
+
+// rotate-shuffle: lane l receives lane (l-1) mod 32's value; lane 0 receives
+// lane 31's, i.e. exactly the carry the NEXT row's lane 0 needs
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ Cpl<T, NT, SPARSE> cpl_rot(const Cpl<T, NT, SPARSE> &c, int src)
+{
+    return cpl_shfl<T, NT, SPARSE>(c, src);
 }
 
 }  // namespace tmg

@@ -1,4 +1,5 @@
-// Single-CTA multilevel engine, exact norms and coarse solves.
+// Single-CTA multilevel engine (coarse tail / whole small solves) and the
+// serial coarse solve.
 //
 // Levels below a few thousand slabs are latency bound: a level pass costs
 // less than a kernel launch.  One CTA per problem therefore runs the rest of
@@ -12,239 +13,11 @@
 // publishes each chunk's last old slab (the only cross-thread dependency),
 // then updates the chunk in place.  Results are independent of the split.
 #pragma once
-#include "tmg_slab.cuh"
+#include "tmg_pairwise.cuh"
+#include "tmg_types.cuh"
 
 namespace tmg {
 
-constexpr int TAIL_THREADS = 512;
-constexpr int MAXLEV = 48;
-
-// ---------------------------------------------------------------------------
-// numpy pairwise summation (np.sum, multigrid.py:459), exact for any n.
-// Serial form for one thread:
-__device__ __forceinline__ double pw_leaf(const double *a, long long n)
-{
-    if (n < 8) {
-        double res = 0.0;
-        for (long long i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
-        return res;
-    }
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    long long i;
-    for (i = 8; i < n - (n % 8); i += 8)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
-}
-
-// serial pairwise over [0, n) with an explicit stack (no device recursion)
-__device__ double pw_serial(const double *a, long long n)
-{
-    // depth <= log2(n / 128) + 1; 40 covers any int64 length
-    struct Node { long long off, len; double left; int state; };
-    Node st[40];
-    int sp = 0;
-    st[0] = {0, n, 0.0, 0};
-    double ret = 0.0;
-    while (sp >= 0) {
-        Node &nd = st[sp];
-        if (nd.len <= 128) {
-            ret = pw_leaf(a + nd.off, nd.len);
-            --sp;
-            continue;
-        }
-        long long n2 = nd.len / 2;
-        n2 -= n2 % 8;
-        if (nd.state == 0) {
-            nd.state = 1;
-            st[sp + 1] = {nd.off, n2, 0.0, 0};
-            ++sp;
-        } else if (nd.state == 1) {
-            nd.left = ret;
-            nd.state = 2;
-            st[sp + 1] = {nd.off + n2, nd.len - n2, 0.0, 0};
-            ++sp;
-        } else {
-            ret = __dadd_rn(nd.left, ret);
-            --sp;
-        }
-    }
-    return ret;
-}
-
-// CTA-wide exact pairwise sum; all threads get the result.  `part` has
-// blockDim.x doubles of shared scratch; blockDim.x must be a power of two.
-__device__ double block_pairwise(const double *a, long long n, double *part)
-{
-    const int T = blockDim.x;
-    int D = 0;
-    while ((1 << D) < T) ++D;
-    const int t = threadIdx.x;
-    long long off = 0, len = n;
-    int d = 0;
-    while (d < D && len > 128) {
-        long long n2 = len / 2;
-        n2 -= n2 % 8;
-        if ((t >> (D - 1 - d)) & 1) { off += n2; len -= n2; }
-        else len = n2;
-        ++d;
-    }
-    const bool owner = (d == D) || ((t & ((1 << (D - d)) - 1)) == 0);
-    if (owner) part[t] = (d == D) ? pw_serial(a + off, len) : pw_leaf(a + off, len);
-    __syncthreads();
-    if (t == 0) {
-        // re-walk the top of the tree, combining owners' partials
-        struct Node { long long len; double left; int d, p, state; };
-        Node st[24];  // depth <= D + 1 <= 11
-        int sp = 0;
-        st[0] = {n, 0.0, 0, 0, 0};
-        double ret = 0.0;
-        while (sp >= 0) {
-            Node &nd = st[sp];
-            if (nd.d == D || nd.len <= 128) {
-                ret = part[nd.p << (D - nd.d)];
-                --sp;
-                continue;
-            }
-            long long n2 = nd.len / 2;
-            n2 -= n2 % 8;
-            if (nd.state == 0) {
-                nd.state = 1;
-                st[sp + 1] = {n2, 0.0, nd.d + 1, nd.p << 1, 0};
-                ++sp;
-            } else if (nd.state == 1) {
-                nd.left = ret;
-                nd.state = 2;
-                st[sp + 1] = {nd.len - n2, 0.0, nd.d + 1, (nd.p << 1) | 1, 0};
-                ++sp;
-            } else {
-                ret = __dadd_rn(nd.left, ret);
-                --sp;
-            }
-        }
-        part[0] = ret;
-    }
-    __syncthreads();
-    double s = part[0];
-    __syncthreads();
-    return s;
-}
-
-// ---------------------------------------------------------------------------
-// per-problem iteration state (multigrid.py:481-496)
-struct ProbState {
-    double tol;
-    int iters;
-    int active;
-    int max_iters;
-    int converged;
-};
-
-// sum of a perfect binary tree of `m` values (m a power of two) per problem,
-// one CTA per problem, then the stopping-rule update.
-//   mode 0: r0 (initialises tol/active), mode 1: after a cycle.
-__global__ void __launch_bounds__(1024)
-    finalize_leaves_kernel(const double *leaves, long long m, ProbState *st, double *hist,
-                           int hist_stride, const double *floor_, double eps, int mode)
-{
-    __shared__ double part[1024];
-    const int b = blockIdx.x;
-    if (mode == 1 && !st[b].active) return;
-    const double *lv = leaves + (size_t)b * m;
-    const int T = blockDim.x;
-    const int t = threadIdx.x;
-    double v = 0.0;
-    long long per = m > T ? m / T : 1;
-    int used = (int)(m > T ? T : m);
-    if (t < used) {
-        // bottom-up perfect tree over [t*per, (t+1)*per)
-        double stack[40];
-        for (long long i = 0; i < per; ++i) {
-            double x = lv[t * per + i];
-            int l = 0;
-            while ((i >> l) & 1) { x = __dadd_rn(stack[l], x); ++l; }
-            stack[l] = x;
-        }
-        int top = 0;
-        while ((1LL << top) < per) ++top;
-        v = stack[top];
-    }
-    part[t] = v;
-    __syncthreads();
-    for (int s = 1; s < used; s <<= 1) {
-        if ((t % (2 * s)) == 0 && t + s < used) part[t] = __dadd_rn(part[t], part[t + s]);
-        __syncthreads();
-    }
-    if (t == 0) {
-        double nrm = __dsqrt_rn(part[0]);
-        ProbState &p = st[b];
-        if (mode == 0) {
-            hist[(size_t)b * hist_stride] = nrm;
-            double e = __dmul_rn(eps, nrm);
-            p.tol = e > floor_[b] ? e : floor_[b];
-            p.iters = 0;
-            p.active = (nrm > p.tol) && (p.max_iters > 0);
-            p.converged = nrm <= p.tol;
-        } else {
-            p.iters += 1;
-            hist[(size_t)b * hist_stride + p.iters] = nrm;
-            p.converged = nrm <= p.tol;
-            p.active = (nrm > p.tol) && (p.iters < p.max_iters);
-        }
-    }
-}
-
-// generic (any n) exact pairwise over per-slab squares
-__global__ void __launch_bounds__(1024)
-    finalize_sq_kernel(const double *sq, long long n, ProbState *st, double *hist, int hist_stride,
-                       const double *floor_, double eps, int mode, double *norm_out)
-{
-    __shared__ double part[1024];
-    const int b = blockIdx.x;
-    if (st && mode == 1 && !st[b].active) return;
-    double s = block_pairwise(sq + (size_t)b * n, n, part);
-    if (threadIdx.x == 0) {
-        double nrm = __dsqrt_rn(s);
-        if (norm_out) norm_out[b] = nrm;
-        if (st) {
-            ProbState &p = st[b];
-            if (mode == 0) {
-                hist[(size_t)b * hist_stride] = nrm;
-                double e = __dmul_rn(eps, nrm);
-                p.tol = e > floor_[b] ? e : floor_[b];
-                p.iters = 0;
-                p.active = (nrm > p.tol) && (p.max_iters > 0);
-                p.converged = nrm <= p.tol;
-            } else {
-                p.iters += 1;
-                hist[(size_t)b * hist_stride + p.iters] = nrm;
-                p.converged = nrm <= p.tol;
-                p.active = (nrm > p.tol) && (p.iters < p.max_iters);
-            }
-        }
-    }
-}
-
-__global__ void active_flags_kernel(const ProbState *st, int *active, int *any, int batch)
-{
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < batch) {
-        int a = st[b].active;
-        active[b] = a;
-        if (a) atomicOr(any, 1);
-    }
-}
-
-__global__ void copy_active_kernel(const ProbState *st, int *active, int batch)
-{
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < batch) active[b] = st[b].active;
-}
 
 // ---------------------------------------------------------------------------
 // coarse solve: block forward substitution (multigrid.py:200-205), one thread
@@ -281,29 +54,6 @@ __global__ void coarse_serial_kernel(const __grid_constant__ LevelC<T, NT> L, co
 
 // ---------------------------------------------------------------------------
 // the single-CTA engine
-
-template <typename T, int NT> struct TailArgs {
-    const LevelC<T, NT> *levels;  // [depth] device array (copied to shared memory)
-    int l0, depth;                // runs levels l0 .. depth-1 (depth-1 = coarsest)
-    long long n[MAXLEV];          // slabs per level
-    long long off[MAXLEV];        // element offset of level l's u (and f) in the store
-    long long store_elems;        // per problem: elements of one level-array set
-    const T *f_in;                // f at l0, [B][n_l0][NT]
-    const T *u_in;                // u at l0 (cycle mode: NULL = zero guess; full: initial guess)
-    T *u_out;                     // u at l0 after the work
-    T *gstore;                    // global level store when not in shared memory
-    int in_smem;
-    int nu1, nu2, gamma, dot_variant;
-    int full;                     // 1: _iterate with norms; 0: n_cycles cycles
-    int n_cycles;
-    // full mode
-    double eps;
-    const double *floor_;
-    int max_iters;
-    double *hist;                 // [B][max_iters+1]
-    ProbState *st;
-    const int *active;
-};
 
 template <typename T, int NT, bool SPARSE> struct Engine {
     const LevelC<T, NT> *L;  // shared copy
@@ -490,12 +240,6 @@ template <typename T, int NT, bool SPARSE> struct Engine {
     }
 };
 
-template <typename T, int NT>
-__host__ __device__ constexpr size_t tail_fixed_smem(int nlev)
-{
-    return sizeof(LevelC<T, NT>) * (size_t)nlev + sizeof(T) * TAIL_THREADS * (NT + 1) +
-           sizeof(double) * TAIL_THREADS + 64;
-}
 
 template <typename T, int NT, bool SPARSE>
 __global__ void __launch_bounds__(TAIL_THREADS)

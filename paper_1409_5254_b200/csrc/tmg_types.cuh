@@ -1,0 +1,50 @@
+// Plain data shared by the host driver and the kernels.
+#pragma once
+#include "tmg_slab.cuh"
+
+namespace tmg {
+
+constexpr int TAIL_THREADS = 512;
+constexpr int MAXLEV = 48;
+
+// per-problem iteration state (multigrid.py:481-496)
+struct ProbState {
+    double tol;
+    int iters;
+    int active;
+    int max_iters;
+    int converged;
+};
+
+template <typename T, int NT> struct TailArgs {
+    const LevelC<T, NT> *levels;  // [depth] device array (copied to shared memory)
+    int l0, depth;                // runs levels l0 .. depth-1 (depth-1 = coarsest)
+    long long n[MAXLEV];          // slabs per level
+    long long off[MAXLEV];        // element offset of level l's u (and f) in the store
+    long long store_elems;        // per problem: elements of one level-array set
+    const T *f_in;                // f at l0, [B][n_l0][NT]
+    const T *u_in;                // u at l0 (cycle mode: NULL = zero guess; full: initial guess)
+    T *u_out;                     // u at l0 after the work
+    T *gstore;                    // global level store when not in shared memory
+    int in_smem;
+    int nu1, nu2, gamma, dot_variant;
+    int full;                     // 1: _iterate with norms; 0: n_cycles cycles
+    int n_cycles;
+    // full mode
+    double eps;
+    const double *floor_;
+    int max_iters;
+    double *hist;                 // [B][max_iters+1]
+    ProbState *st;
+    const int *active;
+};
+
+
+template <typename T, int NT>
+__host__ __device__ constexpr size_t tail_fixed_smem(int nlev)
+{
+    return sizeof(LevelC<T, NT>) * (size_t)nlev + sizeof(T) * TAIL_THREADS * (NT + 1) +
+           sizeof(double) * TAIL_THREADS + 64;
+}
+
+}  // namespace tmg

@@ -271,7 +271,7 @@ def run_gpu_arm(args, w):
         U.zero_()
         if flush is not None:
             flush.zero_()
-        return tmg.solve_batched(hier, F, U, cfg, floors=floors)
+        return tmg.solve_batched(hier, F, U, cfg, floors=floors, inplace=True)
 
     for _ in range(args.warmup):
         _, stats = step()
@@ -300,7 +300,7 @@ def run_gpu_arm(args, w):
         dist.all_reduce(dsum, op=dist.ReduceOp.SUM)
         elapsed, dof = float(tmax.item()), float(dsum.item())
     value = dof / elapsed
-    plan = solver.get_plan(hier, 0, len(hier.levels), solver.level_omegas(hier, cfg, len(hier.levels)),
+    plan = solver.get_plan(hier, 0, len(hier.levels), solver.omegas_for(hier, cfg, len(hier.levels)),
                            cfg, B)
     info = plan.info()
     max_it = max(max(r) for r in iters)
@@ -313,7 +313,8 @@ def run_gpu_arm(args, w):
 
     def e2e_step():
         Fd = F_host.to("cuda", non_blocking=True)
-        Ud, st = tmg.solve_batched(hier, Fd, U0, cfg, floors=floors)
+        U0.zero_()
+        Ud, st = tmg.solve_batched(hier, Fd, U0, cfg, floors=floors, inplace=True)
         U_host.copy_(Ud, non_blocking=True)
         return st
 

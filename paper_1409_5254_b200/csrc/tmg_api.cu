@@ -279,6 +279,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     ~Plan() override
     {
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (sexec) cudaGraphExecDestroy(sexec);
         if (ps) cudaStreamDestroy(ps);
         if (ev_in) cudaEventDestroy(ev_in);
         if (ev_out) cudaEventDestroy(ev_out);
@@ -442,7 +443,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         return 0;
     }
 
-    int enqueue_finalize(int mode, double eps, cudaStream_t s)
+    int enqueue_finalize(int mode, double eps, cudaStream_t s, cudaGraphConditionalHandle h = 0,
+                         bool use_h = false)
     {
         if (leaf_rows0)
             finalize_leaves_kernel<<<(unsigned)B, 1024, 0, s>>>(leaves, nleaves, d_st, d_hist, hist_stride,
@@ -451,20 +453,83 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             finalize_sq_kernel<<<(unsigned)B, 1024, 0, s>>>(sqbuf, n[0], d_st, d_hist, hist_stride, d_floor,
                                                            eps, mode, nullptr);
         CK_LAUNCH("finalize");
-        active_flags_kernel<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(d_st, d_active, d_any, (int)B);
-        CK_LAUNCH("active_flags");
+        set_active_kernel<<<1, 256, 0, s>>>(d_st, d_active, d_any, (int)B, h, use_h ? 1 : 0);
+        CK_LAUNCH("set_active");
         kernels_per_cycle += 2;
         return 0;
     }
 
-    int enqueue_cycle(const void *f, void *u, bool norm, double eps, cudaStream_t s)
+    int enqueue_cycle(const void *f, void *u, bool norm, double eps, cudaStream_t s,
+                      cudaGraphConditionalHandle h = 0, bool use_h = false)
     {
         kernels_per_cycle = 0;
         CKR(enqueue_level(0, f, u, true, norm, s));
-        if (norm) {
-            CK(cudaMemsetAsync(d_any, 0, sizeof(int), s));
-            CKR(enqueue_finalize(1, eps, s));
+        if (norm) CKR(enqueue_finalize(1, eps, s, h, use_h));
+        return 0;
+    }
+
+    // r0 = ||f - L u_init|| and the initial stopping state (multigrid.py:478-481)
+    int enqueue_prefix(const void *f, void *u, double eps, cudaStream_t s, cudaGraphConditionalHandle h = 0,
+                       bool use_h = false)
+    {
+        CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));
+        const bool leaf = leaf_rows0 > 0;
+        StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
+        a.f = (const T *)f;
+        a.u_in = (const T *)u;
+        a.flags = leaf ? SF_NORM_LEAF : SF_NORM_SQ;
+        a.leaf_out = leaves;
+        a.sq_out = sqbuf;
+        if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+        CKR((launch_stream<T, NT>(L[0], a, 0, K_GENERIC, P_GEN, SP, s)));
+        return enqueue_finalize(0, eps, s, h, use_h);
+    }
+
+    // the whole solve as one graph: prefix, then a conditional while node
+    // whose body is one cycle + finalize + set_active (which sets the condition)
+    cudaGraphExec_t sexec = nullptr;
+    const void *s_f = nullptr;
+    void *s_u = nullptr;
+    double s_eps = -1.0;
+    int s_hist = -1;
+
+    int build_solve_graph(const void *f, void *u, double eps)
+    {
+        if (sexec) { cudaGraphExecDestroy(sexec); sexec = nullptr; }
+        cudaGraph_t g;
+        CK(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+        CK(cudaStreamBeginCaptureToGraph(ps, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_prefix(f, u, eps, ps, h, true);
+        cudaGraph_t tmp;
+        cudaError_t ce = cudaStreamEndCapture(ps, &tmp);
+        if (rc) { cudaGraphDestroy(g); return rc; }
+        CK(ce);
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn), leaves_;
+        CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+        for (auto nd : nodes) {
+            size_t nd_out = 0;
+            CK(cudaGraphNodeGetDependentNodes(nd, nullptr, &nd_out));
+            if (nd_out == 0) leaves_.push_back(nd);
         }
+        cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cn;
+        CK(cudaGraphAddNode(&cn, g, leaves_.data(), leaves_.size(), &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(ps, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_cycle(f, u, true, eps, ps, h, true);
+        ce = cudaStreamEndCapture(ps, &tmp);
+        if (rc) { cudaGraphDestroy(g); return rc; }
+        CK(ce);
+        CK(cudaGraphInstantiate(&sexec, g, 0));
+        cudaGraphDestroy(g);
+        s_f = f; s_u = u; s_eps = eps; s_hist = hist_stride;
         return 0;
     }
 
@@ -562,22 +627,12 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.active = nullptr;
             CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");
+        } else if (o.use_graph && !sync_debug() && !getenv("TMG_NO_SOLVE_GRAPH")) {
+            if (!sexec || s_f != f || s_u != u || s_eps != eps || s_hist != hist_stride)
+                CKR(build_solve_graph(f, u, eps));
+            CK(cudaGraphLaunch(sexec, s));
         } else {
-            // r0 = ||f - L u_init|| (norm_at before the loop, multigrid.py:478)
-            CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));
-            {
-                const bool leaf = leaf_rows0 > 0;
-                StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
-                a.f = (const T *)f;
-                a.u_in = (const T *)u;
-                a.flags = leaf ? SF_NORM_LEAF : SF_NORM_SQ;
-                a.leaf_out = leaves;
-                a.sq_out = sqbuf;
-                if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-                CKR((launch_stream<T, NT>(L[0], a, 0, K_GENERIC, P_GEN, SP, s)));
-            }
-            CK(cudaMemsetAsync(d_any, 0, sizeof(int), s));
-            CKR(enqueue_finalize(0, eps, s));
+            CKR(enqueue_prefix(f, u, eps, s));
             CK(cudaMemcpyAsync(h_any, d_any, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             int it = 0;

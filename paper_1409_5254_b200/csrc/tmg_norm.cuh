@@ -91,20 +91,23 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
-__global__ void active_flags_kernel(const ProbState *st, int *active, int *any, int batch)
+// publish the per-problem active flags for the next cycle's kernels and,
+// inside the solve graph, set the while-node condition (any problem active)
+__global__ void __launch_bounds__(256)
+    set_active_kernel(const ProbState *st, int *active, int *any_out, int batch,
+                      cudaGraphConditionalHandle h, int use_handle)
 {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < batch) {
-        int a = st[b].active;
+    int any = 0;
+    for (int b = threadIdx.x; b < batch; b += blockDim.x) {
+        const int a = st[b].active;
         active[b] = a;
-        if (a) atomicOr(any, 1);
+        any |= a;
     }
-}
-
-__global__ void copy_active_kernel(const ProbState *st, int *active, int batch)
-{
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < batch) active[b] = st[b].active;
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) {
+        if (any_out) *any_out = any;
+        if (use_handle) cudaGraphSetConditional(h, any ? 1u : 0u);
+    }
 }
 
 }  // namespace tmg

@@ -78,6 +78,25 @@ __device__ __forceinline__ float divq(float a, float d, float rinv)
     return q2;
 }
 
+// branch-free variant: the caller ORs `bad` over a whole LU solve and redoes
+// the solve with IEEE division when any lane of the warp hit the window edge
+__device__ __forceinline__ double divq_nb(double a, double d, double rinv, unsigned &bad)
+{
+    double q0 = __dmul_rn(a, rinv);
+    double q1 = __fma_rn(__fma_rn(-q0, d, a), rinv, q0);
+    const unsigned e = (unsigned)(__double2hiint(a) >> 20) & 0x7ffu;
+    bad |= (unsigned)(e - 123u >= 1800u);
+    return __fma_rn(__fma_rn(-q1, d, a), rinv, q1);
+}
+__device__ __forceinline__ float divq_nb(float a, float d, float rinv, unsigned &bad)
+{
+    float q0 = __fmul_rn(a, rinv);
+    float q1 = __fmaf_rn(__fmaf_rn(-q0, d, a), rinv, q0);
+    const unsigned e = (__float_as_uint(a) >> 23) & 0xffu;
+    bad |= (unsigned)(e - 28u >= 200u);
+    return __fmaf_rn(__fmaf_rn(-q1, d, a), rinv, q1);
+}
+
 // Per-level constants in the compute type (kernel parameter / shared memory).
 template <typename T, int NT> struct LevelC {
     T A[NT * NT];   // minus_step_matrix  (dg.py:213-215)
@@ -444,6 +463,67 @@ template <typename T, int NT> __device__ __forceinline__ void lu_apply(const Lev
         for (int j = i + 1; j < NT; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
         y[i] = divq(y[i], L.lu[i * NT + i], L.rinv[i]);
     }
+}
+
+// LU solve with branch-free divisions; `bad` flags lanes that need the IEEE path
+template <typename T, int NT>
+__device__ __forceinline__ void lu_apply_nb(const LevelC<T, NT> &L, T (&y)[NT], unsigned &bad)
+{
+#pragma unroll
+    for (int i = 1; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+#pragma unroll
+    for (int i = NT - 1; i >= 0; --i) {
+#pragma unroll
+        for (int j = i + 1; j < NT; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+        y[i] = divq_nb(y[i], L.lu[i * NT + i], L.rinv[i], bad);
+    }
+}
+
+// exact-IEEE LU solve (the rare fallback of lu_apply_nb)
+template <typename T, int NT> __device__ __forceinline__ void lu_apply_ieee(const LevelC<T, NT> &L, T (&y)[NT])
+{
+#pragma unroll
+    for (int i = 1; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+#pragma unroll
+    for (int i = NT - 1; i >= 0; --i) {
+#pragma unroll
+        for (int j = i + 1; j < NT; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+        y[i] = FP<T>::div(y[i], L.lu[i * NT + i]);
+    }
+}
+
+// J independent slabs (one per row of a stage) swept together: two dependency
+// chains per lane hide the fp64 latency of the strictly ordered arithmetic
+template <typename T, int NT, bool SPARSE, int PERM, int J>
+__device__ __forceinline__ void sweep_j(const LevelC<T, NT> &L, T (&u)[J][NT], const T (&f)[J][NT],
+                                        const Cpl<T, NT, SPARSE> (&p)[J], const bool (&hp)[J])
+{
+    T y[J][NT], ys[J][NT];
+    unsigned bad = 0;
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], p[q], hp[q], y[q]);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) ys[q][i] = y[q][i];
+    }
+#pragma unroll
+    for (int q = 0; q < J; ++q) lu_apply_nb<T, NT>(L, y[q], bad);
+    if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+        for (int q = 0; q < J; ++q) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) y[q][i] = ys[q][i];
+            lu_apply_ieee<T, NT>(L, y[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < J; ++q)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) u[q][i] = FP<T>::add(FP<T>::mul(y[q][i], L.omega), u[q][i]);
 }
 
 template <typename T, int NT, bool SPARSE, int PERM>

@@ -28,7 +28,7 @@
 namespace tmg {
 
 constexpr int SW_WARPS = 8;   // warps per CTA
-constexpr int SW_STAGES = 4;  // ring stages per warp
+constexpr int SW_STAGES = 3;  // ring stages per warp
 constexpr int SW_GROUP = 2;   // rows per stage
 
 enum StreamFlags : int {
@@ -115,12 +115,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-template <typename T, int NT> struct RowLayout {
+template <typename T, int NT, bool WITH_C> struct RowLayout {
     static constexpr int ROW = 32 * NT;   // elements of one fine row
     static constexpr int HALF = 16 * NT;  // elements of the matching coarse half-row
     static constexpr int OFF_F = SW_GROUP * ROW;
     static constexpr int OFF_C = 2 * SW_GROUP * ROW;
-    static constexpr int STAGE = SW_GROUP * (2 * ROW + HALF);
+    static constexpr int STAGE = SW_GROUP * (2 * ROW + (WITH_C ? HALF : 0));
     // per-warp copy of (R1, R2) for n_t >= 3 (R2 padded by 2 elements so the
     // even and odd half-warps read different banks)
     static constexpr int RELEMS = NT >= 3 ? 2 * NT * NT + 2 : 0;
@@ -132,12 +132,17 @@ template <typename T, int NT> struct RowLayout {
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * SW_WARPS;
 };
 
+template <int KIND> struct KindProlongs { static constexpr bool value = KIND != K_DOWN; };
+
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct Streamer {
     using C = Cpl<T, NT, SPARSE>;
     static constexpr int CF = KIND == K_DOWN ? (SF_RESTRICT | SF_WRITE_U)
                               : KIND == K_UP ? (SF_PROLONG | SF_WRITE_U)
                               : KIND == K_UPNORM ? (SF_PROLONG | SF_WRITE_U | SF_NORM_LEAF)
                                                  : 0;
+    // rows swept jointly per lane (two dependency chains hide fp64 latency);
+    // larger blocks have enough independent work per row already
+    static constexpr int J = NT <= 2 ? 2 : 1;
     const LevelC<T, NT> &L;
     const StreamArgs<T> &a;
     int lane;
@@ -161,90 +166,127 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         return has(SF_RESTRICT) || has(SF_NORM_LEAF) || has(SF_NORM_SQ) || has(SF_WRITE_R);
     }
 
-    __device__ __forceinline__ void exchange(const T (&u)[NT], int k, C &prev)
+    // predecessor data for JJ consecutive rows at sweep k (rotate-shuffle + carry)
+    template <int JJ>
+    __device__ __forceinline__ void exchange(const T (&u)[JJ][NT], int k, C (&prev)[JJ])
     {
-        C own = make_cpl<T, NT, SPARSE>(L, u);
-        C x = cpl_shfl<T, NT, SPARSE>(own, (lane + 31) & 31);
-        prev = x;
-        cpl_select<T, NT, SPARSE>(prev, carry[k], lane == 0);
-        carry[k] = x;
+        C x[JJ];
+#pragma unroll
+        for (int q = 0; q < JJ; ++q) {
+            C own = make_cpl<T, NT, SPARSE>(L, u[q]);
+            x[q] = cpl_shfl<T, NT, SPARSE>(own, (lane + 31) & 31);
+        }
+        prev[0] = x[0];
+        cpl_select<T, NT, SPARSE>(prev[0], carry[k], lane == 0);
+#pragma unroll
+        for (int q = 1; q < JJ; ++q) {
+            prev[q] = x[q];
+            cpl_select<T, NT, SPARSE>(prev[q], x[q - 1], lane == 0);
+        }
+        carry[k] = x[JJ - 1];
     }
 
-    // one row; INTERIOR: all 32 slabs exist and none is slab 0 of the problem
-    template <bool INTERIOR>
-    __device__ __forceinline__ void row(T (&u)[NT], const T (&f)[NT], const T (&uc)[NT], long long slab,
-                                        long long row_idx, bool warm, int b)
+    // JJ rows starting at slab0 (this lane's slab in the first row);
+    // INTERIOR: every slab exists and none is slab 0 of the problem.
+    // Rows q >= nrow are beyond the chunk: computed but never stored.
+    template <bool INTERIOR, int JJ>
+    __device__ __forceinline__ void rows(T (&u)[JJ][NT], const T (&f)[JJ][NT], const T (&uc)[JJ][NT],
+                                         long long slab0, long long row_idx0, int nrow, bool warm, int b)
     {
-        const bool valid = INTERIOR || slab < a.n;
-        const bool hp = INTERIOR || slab > 0;
-        if (has(SF_PROLONG)) {
-            if (INTERIOR || slab < 2 * nc) {
-                if constexpr (RREG) prolong_reg<T, NT>(Rm, uc, u);
-                else prolong_ptr<T, NT>(Rs, uc, u);
+        bool valid[JJ], hp[JJ];
+#pragma unroll
+        for (int q = 0; q < JJ; ++q) {
+            const long long sl = slab0 + 32 * q;
+            valid[q] = INTERIOR || (q < nrow && sl < a.n);
+            hp[q] = INTERIOR || sl > 0;
+            if (has(SF_PROLONG)) {
+                if (INTERIOR || sl < 2 * nc) {
+                    if constexpr (RREG) prolong_reg<T, NT>(Rm, uc[q], u[q]);
+                    else prolong_ptr<T, NT>(Rs, uc[q], u[q]);
+                }
             }
         }
 #pragma unroll
         for (int k = 0; k < NU; ++k) {
-            C prev;
-            exchange(u, k, prev);
-            sweep_p<T, NT, SPARSE, PERM>(L, u, f, prev, hp);
+            C prev[JJ];
+            exchange<JJ>(u, k, prev);
+            sweep_j<T, NT, SPARSE, PERM, JJ>(L, u, f, prev, hp);
         }
         if (need_r()) {
-            C prev;
-            exchange(u, NU, prev);
+            C prev[JJ];
+            exchange<JJ>(u, NU, prev);
             if (!warm) {
-                T r[NT];
-                residual<T, NT, SPARSE>(L, u, f, prev, hp, r);
-                if (has(SF_WRITE_R) && valid) store_slab<T, NT>(a.r_out + ((size_t)b * a.n + slab) * NT, r);
-                if (has(SF_RESTRICT)) {
-                    T p[NT], q[NT];
-                    if constexpr (RREG) restrict_reg<T, NT>(Rm, r, p);
-                    else restrict_ptr<T, NT>(Rs, r, p);
 #pragma unroll
-                    for (int i = 0; i < NT; ++i) q[i] = __shfl_down_sync(0xffffffffu, p[i], 1);
+                for (int q = 0; q < JJ; ++q) {
+                    const long long sl = slab0 + 32 * q;
+                    T r[NT];
+                    residual<T, NT, SPARSE>(L, u[q], f[q], prev[q], hp[q], r);
+                    if (has(SF_WRITE_R) && valid[q]) store_slab<T, NT>(a.r_out + ((size_t)b * a.n + sl) * NT, r);
+                    if (has(SF_RESTRICT)) {
+                        T p[NT], qq[NT];
+                        if constexpr (RREG) restrict_reg<T, NT>(Rm, r, p);
+                        else restrict_ptr<T, NT>(Rs, r, p);
 #pragma unroll
-                    for (int i = 0; i < NT; ++i) p[i] = FP<T>::add(p[i], q[i]);
-                    const long long cidx = slab >> 1;
-                    if (!(lane & 1) && (INTERIOR || cidx < nc))
-                        store_slab<T, NT>(a.fc + ((size_t)b * nc + cidx) * NT, p);
-                }
-                if (has(SF_NORM_SQ)) {
-                    if (valid) a.sq_out[(size_t)b * a.n + slab] = (double)sqnorm<T, NT>(r);
-                }
-                if (has(SF_NORM_LEAF)) {
-                    // numpy pairwise leaf (np.sum, multigrid.py:459): 8 accumulators,
-                    // accumulator j sums elements j, j+8, j+16, ... of the leaf in order
-                    T sq = sqnorm<T, NT>(r);
-                    T v1 = __shfl_down_sync(0xffffffffu, sq, 8);
-                    T v2 = __shfl_down_sync(0xffffffffu, sq, 16);
-                    T v3 = __shfl_down_sync(0xffffffffu, sq, 24);
-                    leaf_acc = (leaf_q == 0) ? sq : FP<T>::add(leaf_acc, sq);
-                    leaf_acc = FP<T>::add(leaf_acc, v1);
-                    leaf_acc = FP<T>::add(leaf_acc, v2);
-                    leaf_acc = FP<T>::add(leaf_acc, v3);
-                    if (leaf_q == a.leaf_rows - 1) {
-                        T t1 = FP<T>::add(leaf_acc, __shfl_down_sync(0xffffffffu, leaf_acc, 1));
-                        T t2 = FP<T>::add(t1, __shfl_down_sync(0xffffffffu, t1, 2));
-                        T t3 = FP<T>::add(t2, __shfl_down_sync(0xffffffffu, t2, 4));
-                        const long long nleaves = a.n / (32LL * a.leaf_rows);
-                        if (lane == 0) a.leaf_out[(size_t)b * nleaves + row_idx / a.leaf_rows] = (double)t3;
-                        leaf_q = 0;
-                    } else {
-                        leaf_q += 1;
+                        for (int i = 0; i < NT; ++i) qq[i] = __shfl_down_sync(0xffffffffu, p[i], 1);
+#pragma unroll
+                        for (int i = 0; i < NT; ++i) p[i] = FP<T>::add(p[i], qq[i]);
+                        const long long cidx = sl >> 1;
+                        if (!(lane & 1) && (INTERIOR || (valid[q] && cidx < nc)))
+                            store_slab<T, NT>(a.fc + ((size_t)b * nc + cidx) * NT, p);
+                    }
+                    if (has(SF_NORM_SQ)) {
+                        if (valid[q]) a.sq_out[(size_t)b * a.n + sl] = (double)sqnorm<T, NT>(r);
+                    }
+                    if (has(SF_NORM_LEAF) && (INTERIOR || q < nrow)) {
+                        // numpy pairwise leaf (np.sum, multigrid.py:459): accumulator
+                        // j sums leaf elements j, j+8, j+16, ... in order
+                        T sq = sqnorm<T, NT>(r);
+                        T v1 = __shfl_down_sync(0xffffffffu, sq, 8);
+                        T v2 = __shfl_down_sync(0xffffffffu, sq, 16);
+                        T v3 = __shfl_down_sync(0xffffffffu, sq, 24);
+                        leaf_acc = (leaf_q == 0) ? sq : FP<T>::add(leaf_acc, sq);
+                        leaf_acc = FP<T>::add(leaf_acc, v1);
+                        leaf_acc = FP<T>::add(leaf_acc, v2);
+                        leaf_acc = FP<T>::add(leaf_acc, v3);
+                        if (leaf_q == a.leaf_rows - 1) {
+                            T t1 = FP<T>::add(leaf_acc, __shfl_down_sync(0xffffffffu, leaf_acc, 1));
+                            T t2 = FP<T>::add(t1, __shfl_down_sync(0xffffffffu, t1, 2));
+                            T t3 = FP<T>::add(t2, __shfl_down_sync(0xffffffffu, t2, 4));
+                            const long long nleaves = a.n / (32LL * a.leaf_rows);
+                            if (lane == 0)
+                                a.leaf_out[(size_t)b * nleaves + (row_idx0 + q) / a.leaf_rows] = (double)t3;
+                            leaf_q = 0;
+                        } else {
+                            leaf_q += 1;
+                        }
                     }
                 }
             }
         }
-        if (has(SF_WRITE_U) && !warm && valid) store_slab<T, NT>(a.u_out + ((size_t)b * a.n + slab) * NT, u);
+        if (has(SF_WRITE_U) && !warm) {
+#pragma unroll
+            for (int q = 0; q < JJ; ++q)
+                if (valid[q]) store_slab<T, NT>(a.u_out + ((size_t)b * a.n + slab0 + 32 * q) * NT, u[q]);
+        }
     }
 };
+
+template <typename T, int NT>
+__device__ __forceinline__ void load_row(const T *src, T (&x)[NT], bool vec)
+{
+    if (vec) load_slab<T, NT>(src, x);
+    else load_slab_scalar<T, NT>(src, x);
+}
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM>
 __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
     stream_kernel(const __grid_constant__ LevelC<T, NT> L, const __grid_constant__ StreamArgs<T> a)
 {
-    using Lay = RowLayout<T, NT>;
+    constexpr bool WITH_C = KindProlongs<KIND>::value;
+    using Lay = RowLayout<T, NT, WITH_C>;
     using S = Streamer<T, NT, NU, SPARSE, KIND, PERM>;
+    constexpr int J = S::J;
+    constexpr int G = SW_GROUP;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -260,10 +302,10 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
     const long long nrows = (n + 31) >> 5;
     const long long row0 = chunk * a.rows_per_chunk;
     const int rows = (int)min((long long)a.rows_per_chunk, nrows - row0);
-    const int ngroups = (rows + SW_GROUP - 1) / SW_GROUP;
+    const int ngroups = (rows + G - 1) / G;
     const bool zero_guess = a.flags & SF_ZERO_GUESS;
     const bool tma = a.flags & SF_TMA;
-    const bool prolong = st.has(SF_PROLONG);
+    const bool prolong = WITH_C && st.has(SF_PROLONG);
 
     const T *fb = a.f + (size_t)b * n * NT;
     const T *ub = zero_guess ? nullptr : a.u_in + (size_t)b * n * NT;
@@ -292,9 +334,9 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
     st.leaf_acc = T(0);
     st.leaf_q = 0;
 
-    // a group goes through the ring iff it consists of SW_GROUP whole rows
+    // a group goes through the ring iff it consists of G whole rows
     auto group_tma = [&](int g) -> bool {
-        return tma && (g + 1) * SW_GROUP <= rows && (row0 + (long long)(g + 1) * SW_GROUP) * 32 <= n;
+        return tma && (g + 1) * G <= rows && (row0 + (long long)(g + 1) * G) * 32 <= n;
     };
     uint64_t pol = 0;
     if (lane == 0 && tma) {
@@ -308,9 +350,9 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
         if (!group_tma(g)) return;
         T *stg = ring + (size_t)(g % SW_STAGES) * Lay::STAGE;
         uint64_t *bar = &bars[g % SW_STAGES];
-        const long long s0 = (row0 + (long long)g * SW_GROUP) * 32;
-        const uint32_t bytes = (uint32_t)(SW_GROUP * Lay::ROW * sizeof(T));
-        const uint32_t cbytes = prolong ? (uint32_t)(SW_GROUP * Lay::HALF * sizeof(T)) : 0u;
+        const long long s0 = (row0 + (long long)g * G) * 32;
+        const uint32_t bytes = (uint32_t)(G * Lay::ROW * sizeof(T));
+        const uint32_t cbytes = prolong ? (uint32_t)(G * Lay::HALF * sizeof(T)) : 0u;
         mbar_expect_tx(bar, bytes * (zero_guess ? 1u : 2u) + cbytes);
         bulk_g2s(stg + Lay::OFF_F, fb + s0 * NT, bytes, bar, pol);
         if (!zero_guess) bulk_g2s(stg, ub + s0 * NT, bytes, bar, pol);
@@ -319,59 +361,65 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
     if (lane == 0 && tma)
         for (int g = 0; g < ngroups && g < SW_STAGES; ++g) issue(g);
 
-    // warm-up row (the 32 slabs before the chunk): carries only, no outputs
+    // warm-up: the J rows before the chunk, for the carries only
     if (row0 > 0) {
-        const long long slab = (row0 - 1) * 32 + lane;
-        T u[NT], f[NT], uc[NT];
-        zero_slab<T, NT>(u);
-        zero_slab<T, NT>(uc);
-        if (tma) {
-            load_slab<T, NT>(fb + slab * NT, f);
-            if (!zero_guess) load_slab<T, NT>(ub + slab * NT, u);
-            if (prolong) load_slab<T, NT>(ucb + (slab >> 1) * NT, uc);
-        } else {
-            load_slab_scalar<T, NT>(fb + slab * NT, f);
-            if (!zero_guess) load_slab_scalar<T, NT>(ub + slab * NT, u);
-            if (prolong) load_slab_scalar<T, NT>(ucb + (slab >> 1) * NT, uc);
+        T u[J][NT], f[J][NT], uc[J][NT];
+        const long long wr0 = row0 - J;
+#pragma unroll
+        for (int q = 0; q < J; ++q) {
+            const long long sl = (wr0 + q) * 32 + lane;
+            zero_slab<T, NT>(u[q]);
+            zero_slab<T, NT>(uc[q]);
+            load_row<T, NT>(fb + sl * NT, f[q], tma);
+            if (!zero_guess) load_row<T, NT>(ub + sl * NT, u[q], tma);
+            if (prolong) load_row<T, NT>(ucb + (sl >> 1) * NT, uc[q], tma);
         }
-        if (row0 - 1 > 0) st.template row<true>(u, f, uc, slab, row0 - 1, true, b);
-        else st.template row<false>(u, f, uc, slab, row0 - 1, true, b);
+        if (wr0 > 0) st.template rows<true, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b);
+        else st.template rows<false, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b);
     }
 
     for (int g = 0; g < ngroups; ++g) {
         const bool gt = group_tma(g);
         const T *stg = ring + (size_t)(g % SW_STAGES) * Lay::STAGE;
+        const long long r0g = row0 + (long long)g * G;
+        const int nrow = min(G, rows - g * G);
+        const bool interior = r0g > 0 && (r0g + G) * 32 <= n && nrow == G;
         if (gt) mbar_wait(&bars[g % SW_STAGES], (uint32_t)((g / SW_STAGES) & 1));
 #pragma unroll
-        for (int q = 0; q < SW_GROUP; ++q) {
-            const int rr = g * SW_GROUP + q;
-            if (rr >= rows) break;
-            const long long row_idx = row0 + rr;
-            const long long slab = row_idx * 32 + lane;
-            T u[NT], f[NT], uc[NT];
-            if (gt) {
-                load_slab<T, NT>(stg + Lay::OFF_F + q * Lay::ROW + lane * NT, f);
-                if (zero_guess) zero_slab<T, NT>(u);
-                else load_slab<T, NT>(stg + q * Lay::ROW + lane * NT, u);
-                if (prolong) load_slab<T, NT>(stg + Lay::OFF_C + q * Lay::HALF + (lane >> 1) * NT, uc);
-                else zero_slab<T, NT>(uc);
-            } else {
-                zero_slab<T, NT>(u);
-                zero_slab<T, NT>(f);
-                zero_slab<T, NT>(uc);
-                if (slab < n) {
-                    load_slab_scalar<T, NT>(fb + slab * NT, f);
-                    if (!zero_guess) load_slab_scalar<T, NT>(ub + slab * NT, u);
-                    if (prolong && slab < 2 * st.nc) load_slab_scalar<T, NT>(ucb + (slab >> 1) * NT, uc);
+        for (int q0 = 0; q0 < G; q0 += J) {
+            T u[J][NT], f[J][NT], uc[J][NT];
+#pragma unroll
+            for (int q = 0; q < J; ++q) {
+                const int qq = q0 + q;
+                const long long sl = (r0g + qq) * 32 + lane;
+                if (gt) {
+                    load_slab<T, NT>(stg + Lay::OFF_F + qq * Lay::ROW + lane * NT, f[q]);
+                    if (zero_guess) zero_slab<T, NT>(u[q]);
+                    else load_slab<T, NT>(stg + qq * Lay::ROW + lane * NT, u[q]);
+                    if (prolong) load_slab<T, NT>(stg + Lay::OFF_C + qq * Lay::HALF + (lane >> 1) * NT, uc[q]);
+                    else zero_slab<T, NT>(uc[q]);
+                } else {
+                    zero_slab<T, NT>(u[q]);
+                    zero_slab<T, NT>(f[q]);
+                    zero_slab<T, NT>(uc[q]);
+                    if (qq < nrow && sl < n) {
+                        load_slab_scalar<T, NT>(fb + sl * NT, f[q]);
+                        if (!zero_guess) load_slab_scalar<T, NT>(ub + sl * NT, u[q]);
+                        if (prolong && sl < 2 * st.nc) load_slab_scalar<T, NT>(ucb + (sl >> 1) * NT, uc[q]);
+                    }
                 }
             }
-            if (q == SW_GROUP - 1 || rr + 1 >= rows) {
+            if (q0 + J >= G) {
                 // the stage is fully read: hand it back to the copy engine
                 __syncwarp();
                 if (gt && lane == 0 && g + SW_STAGES < ngroups) issue(g + SW_STAGES);
             }
-            if (row_idx > 0 && (row_idx + 1) * 32 <= n) st.template row<true>(u, f, uc, slab, row_idx, false, b);
-            else st.template row<false>(u, f, uc, slab, row_idx, false, b);
+            if (q0 < nrow) {
+                if (interior)
+                    st.template rows<true, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, J, false, b);
+                else
+                    st.template rows<false, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, nrow - q0, false, b);
+            }
         }
     }
 }

@@ -92,8 +92,9 @@ class DevicePlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and nat._lib is not None:
-            nat._lib.tmg_plan_destroy(h)
+        lib = getattr(nat, "_lib", None) if nat is not None else None
+        if h is not None and h.value and lib is not None:
+            lib.tmg_plan_destroy(h)
             self._h = None
 
     def cycles(self, f_dev, u_dev, n_cycles: int = 1):
@@ -123,6 +124,16 @@ class DevicePlan:
         nat.check(nat.load().tmg_plan_info(self._h, ctypes.byref(k), ctypes.byref(s),
                                            ctypes.byref(t)))
         return {"kernels_per_cycle": k.value, "tail_level": t.value}
+
+
+def omegas_for(hier, config, depth):
+    """Per-level damping, cached on the hierarchy (alpha needs a small complex
+    solve per level; multigrid.py:339-341)."""
+    cache = hier.__dict__.setdefault("_tmg_omegas", {})
+    key = (repr(config.damping), depth)
+    if key not in cache:
+        cache[key] = level_omegas(hier, config, depth)
+    return cache[key]
 
 
 def get_plan(hier, level0, depth, omegas, config, batch, dtype=nat.F64):
@@ -167,7 +178,7 @@ def block_jacobi_sweep(ops, u, f, omega: float, nu: int = 1):
 def _cycle_api(hier, level, depth_total, u, f, config):
     ud, was_t = _dev(u)
     fd, _ = _dev(f)
-    omegas = level_omegas(hier, config, depth_total)[level:]
+    omegas = omegas_for(hier, config, depth_total)[level:]
     plan = get_plan(hier, level, depth_total - level, omegas, config, 1)
     out = ud.clone()
     plan.cycles(fd, out, 1)
@@ -233,7 +244,7 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
     ud, _ = _dev(u_init)
     ud = ud.clone()
     floor = _floor_of(f)
-    omegas = level_omegas(hier, config, depth)
+    omegas = omegas_for(hier, config, depth)
     plan = get_plan(hier, 0, depth, omegas, config, 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -247,10 +258,11 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
     return _out(ud, was_t), stats
 
 
-def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None):
+def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None, inplace=False):
     """B independent problems sharing hier's operator: F, U0 of shape
     (B, N, n_t).  Each problem follows the reference stopping rule on its own
-    (exactly as B separate ``solve`` calls).  Returns (U, [SolveStats])."""
+    (exactly as B separate ``solve`` calls).  Returns (U, [SolveStats]).
+    ``inplace=True`` (device tensors only) overwrites U0 with the solution."""
     config = config or CycleConfig()
     depth = depth_of(hier, config)
     if depth < 2:
@@ -262,13 +274,14 @@ def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None):
         Ud = torch.zeros_like(Fd)
     else:
         Ud, _ = _dev(U0)
-        Ud = Ud.clone()
+        if not (inplace and torch.is_tensor(U0) and Ud.data_ptr() == U0.data_ptr()):
+            Ud = Ud.clone()
     if floors is None:
         if torch.is_tensor(F):
             floors = [1e-12 * float(v) for v in torch.linalg.norm(Fd.reshape(B, -1), dim=1).cpu()]
         else:
             floors = [1e-12 * float(np.linalg.norm(F[b])) for b in range(B)]
-    omegas = level_omegas(hier, config, depth)
+    omegas = omegas_for(hier, config, depth)
     plan = get_plan(hier, 0, depth, omegas, config, B)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -295,7 +308,7 @@ def measure_convergence_factor(hier, config: CycleConfig = None) -> float:
     torch = _torch()
     fd, _ = _dev(f)
     ud, _ = _dev(random_initial_guess(hier, config.seed))
-    omegas = level_omegas(hier, config, 2)
+    omegas = omegas_for(hier, config, 2)
     plan = get_plan(hier, 0, 2, omegas, config, 1)
     it, norms, conv = plan.solve(fd, ud, [0.0], config.eps, min(config.max_iters, 250))
     k = int(it[0])

@@ -141,6 +141,14 @@ int tmg_plan_cycles(tmg_plan *plan, const void *f, void *u, int n_cycles, void *
 int tmg_plan_solve(tmg_plan *plan, const void *f, void *u, const double *floor_per_problem,
                    double eps, int max_iters, void *stream);
 
+/* Host-buffer form of tmg_plan_solve -- the call a host-side binding of the
+ * reference makes (numpy arrays in, numpy arrays out): f_host and u_host are
+ * host arrays [batch][n_slabs][n_t] (pinned memory gives full PCIe speed).
+ * Copies f and the initial guess in, solves, copies the solution back into
+ * u_host.  Device buffers are owned by the plan.  Blocks until done. */
+int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, void *u_host, const double *floor_per_problem,
+                        double eps, int max_iters);
+
 /* Results of the last tmg_plan_solve (host arrays):
  * iterations[batch], norms[batch * (max_iters + 1)] (first iterations[b]+1
  * valid per problem), converged[batch]. */

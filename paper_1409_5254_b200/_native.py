@@ -102,8 +102,8 @@ _lib = None
 
 EXPORTS = ("tmg_last_error", "tmg_version", "tmg_device_check", "tmg_sweep", "tmg_residual",
            "tmg_down", "tmg_up", "tmg_coarse_solve", "tmg_resid_norm", "tmg_plan_create",
-           "tmg_plan_destroy", "tmg_plan_cycles", "tmg_plan_solve", "tmg_plan_stats",
-           "tmg_plan_info")
+           "tmg_plan_destroy", "tmg_plan_cycles", "tmg_plan_solve", "tmg_plan_solve_host",
+           "tmg_plan_stats", "tmg_plan_info")
 
 
 def load():
@@ -131,6 +131,7 @@ def load():
     L.tmg_plan_destroy.argtypes = [vp]
     L.tmg_plan_cycles.argtypes = [vp, vp, vp, ci, vp]
     L.tmg_plan_solve.argtypes = [vp, vp, vp, dp, ctypes.c_double, ci, vp]
+    L.tmg_plan_solve_host.argtypes = [vp, vp, vp, dp, ctypes.c_double, ci]
     L.tmg_plan_stats.argtypes = [vp, i32p, dp, i32p]
     L.tmg_plan_info.argtypes = [vp, i32p, i32p, i32p]
     for name in EXPORTS:

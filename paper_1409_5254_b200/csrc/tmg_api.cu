@@ -228,6 +228,7 @@ struct PlanBase {
     virtual int cycles(const void *f, void *u, int n_cycles, cudaStream_t s) = 0;
     virtual int solve(const void *f, void *u, const double *floor_, double eps, int max_iters,
                       cudaStream_t s) = 0;
+    virtual int solve_host(const void *f, void *u, const double *floor_, double eps, int max_iters) = 0;
     virtual int stats(int32_t *it, double *norms, int32_t *conv) const = 0;
     virtual int info(int32_t *kpc, int32_t *sl, int32_t *tl) const = 0;
 };
@@ -287,6 +288,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         for (auto p : uB) cudaFree(p);
         for (auto p : fl) cudaFree(p);
         cudaFree(d_levels);
+        cudaFree(d_fh);
+        cudaFree(d_uh);
         cudaFree(gstore);
         cudaFree(leaves);
         cudaFree(sqbuf);
@@ -577,6 +580,23 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         CKR(enter(user));
         CKR(solve_on(f, u, floor_, eps, max_iters, ps));
         return leave(user);
+    }
+
+    T *d_fh = nullptr, *d_uh = nullptr;  // device copies for the host-buffer entry point
+
+    int solve_host(const void *f, void *u, const double *floor_, double eps, int max_iters) override
+    {
+        const size_t bytes = sizeof(T) * n[0] * NT * B;
+        if (!d_fh) {
+            CK(cudaMalloc(&d_fh, bytes));
+            CK(cudaMalloc(&d_uh, bytes));
+        }
+        CK(cudaMemcpyAsync(d_fh, f, bytes, cudaMemcpyHostToDevice, ps));
+        CK(cudaMemcpyAsync(d_uh, u, bytes, cudaMemcpyHostToDevice, ps));
+        CKR(solve_on(d_fh, d_uh, floor_, eps, max_iters, ps));
+        CK(cudaMemcpyAsync(u, d_uh, bytes, cudaMemcpyDeviceToHost, ps));
+        CK(cudaStreamSynchronize(ps));
+        return 0;
     }
 
     int cycles_on(const void *f, void *u, int nc, cudaStream_t s)
@@ -961,6 +981,14 @@ int tmg_plan_solve(tmg_plan *plan, const void *f, void *u, const double *floor_p
     if (!plan) return fail(TMG_E_ARG, "NULL plan");
     if (!(eps > 0.0 && eps < 1.0)) return fail(TMG_E_ARG, "eps must lie in (0, 1)");
     return plan->impl->solve(f, u, floor_per_problem, eps, max_iters, (cudaStream_t)stream);
+}
+
+int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, void *u_host, const double *floor_per_problem,
+                        double eps, int max_iters)
+{
+    if (!plan) return fail(TMG_E_ARG, "NULL plan");
+    if (!(eps > 0.0 && eps < 1.0)) return fail(TMG_E_ARG, "eps must lie in (0, 1)");
+    return plan->impl->solve_host(f_host, u_host, floor_per_problem, eps, max_iters);
 }
 
 int tmg_plan_stats(const tmg_plan *plan, int32_t *iterations, double *norms, int32_t *converged)

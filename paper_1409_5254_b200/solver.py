@@ -60,6 +60,38 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _is_host(x) -> bool:
+    if isinstance(x, np.ndarray):
+        return True
+    try:
+        import torch
+        return torch.is_tensor(x) and not x.is_cuda
+    except ImportError:
+        return False
+
+
+def _host_ptr(x) -> int:
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _host_array(x, copy: bool):
+    """C-contiguous float64 host array (numpy, or a CPU torch tensor kept as is)."""
+    if isinstance(x, np.ndarray):
+        return np.array(x, dtype=np.float64, order="C", copy=True) if copy else \
+            np.ascontiguousarray(x, dtype=np.float64)
+    import torch
+    if torch.is_tensor(x):
+        t = x.to(torch.float64).contiguous()
+        return t.clone() if copy and t.data_ptr() == x.data_ptr() else t
+    return np.array(x, dtype=np.float64, order="C", copy=True)
+
+
+def _check_device():
+    nat.check(nat.load().tmg_device_check(0), "timemg_b200 needs a CUDA device (B200, sm_100a)")
+
+
 def _out(t, was_torch):
     if was_torch:
         return t
@@ -107,6 +139,19 @@ class DevicePlan:
             self._h, _ptr(f_dev), _ptr(u_dev),
             floors.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(eps), int(max_iters),
             _stream()), "tmg_plan_solve")
+        return self._stats(max_iters)
+
+    def solve_host(self, f_host, u_host, floors, eps: float, max_iters: int):
+        """Host buffers (numpy or CPU torch, ideally pinned) in and out: the
+        C ABI copies in, solves and copies the solution back into u_host."""
+        floors = np.ascontiguousarray(floors, dtype=np.float64)
+        nat.check(nat.load().tmg_plan_solve_host(
+            self._h, ctypes.c_void_p(_host_ptr(f_host)), ctypes.c_void_p(_host_ptr(u_host)),
+            floors.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(eps), int(max_iters)),
+            "tmg_plan_solve_host")
+        return self._stats(max_iters)
+
+    def _stats(self, max_iters):
         it = np.zeros(self.batch, dtype=np.int32)
         conv = np.zeros(self.batch, dtype=np.int32)
         norms = np.zeros(self.batch * (max_iters + 1))
@@ -114,8 +159,7 @@ class DevicePlan:
             self._h, it.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
             norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
             conv.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), "tmg_plan_stats")
-        norms = norms.reshape(self.batch, max_iters + 1)
-        return it, norms, conv
+        return it, norms.reshape(self.batch, max_iters + 1), conv
 
     def info(self):
         k = ctypes.c_int32()
@@ -231,10 +275,25 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
     Returns (u, SolveStats); non-convergence is a flag, not an exception."""
     config = config or CycleConfig()
     depth = depth_of(hier, config)
-    torch = _torch()
-    fd, was_t = _dev(f)
     if u_init is None:
         u_init = random_initial_guess(hier, config.seed)
+    if depth >= 2 and _is_host(f):
+        # numpy (host) arrays: the C ABI's host-buffer entry point, no torch
+        _check_device()
+        fh = _host_array(f, copy=False)
+        uh = _host_array(u_init, copy=True)
+        floor = 1e-12 * float(np.linalg.norm(np.asarray(f, dtype=np.float64)))
+        plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, 1)
+        t0 = time.perf_counter()
+        it, norms, conv = plan.solve_host(fh, uh, [floor], config.eps, config.max_iters)
+        elapsed = time.perf_counter() - t0
+        k = int(it[0])
+        hist = [float(v) for v in norms[0, :k + 1]]
+        return uh, SolveStats(iterations=k, residual_norms=hist, factor=max_ratio(hist),
+                              times=_times(elapsed), converged=bool(conv[0]), seed=config.seed,
+                              workers=config.workers)
+    torch = _torch()
+    fd, was_t = _dev(f)
     if depth < 2:
         u = _forward_solve_dev(hier.finest.ops, hier.finest.n_steps, fd, config)
         stats = SolveStats(iterations=0, residual_norms=[0.0], factor=float("nan"),
@@ -267,6 +326,23 @@ def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None, inp
     depth = depth_of(hier, config)
     if depth < 2:
         raise ValueError("solve_batched needs at least 2 levels")
+    if _is_host(F):
+        # host buffers (numpy / CPU torch, ideally pinned): copies inside the C ABI
+        _check_device()
+        Fh = _host_array(F, copy=False)
+        B = Fh.shape[0]
+        if U0 is None:
+            Uh = np.zeros(tuple(Fh.shape))
+        else:
+            Uh = _host_array(U0, copy=not inplace)
+        if floors is None:
+            floors = [1e-12 * float(np.linalg.norm(np.asarray(Fh[b], dtype=np.float64)))
+                      for b in range(B)]
+        plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, B)
+        t0 = time.perf_counter()
+        it, norms, conv = plan.solve_host(Fh, Uh, floors, config.eps, config.max_iters)
+        elapsed = time.perf_counter() - t0
+        return Uh, _batched_stats(it, norms, conv, elapsed, config)
     torch = _torch()
     Fd, was_t = _dev(F)
     B = Fd.shape[0]
@@ -287,14 +363,18 @@ def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None, inp
     t0 = time.perf_counter()
     it, norms, conv = plan.solve(Fd, Ud, floors, config.eps, config.max_iters)
     elapsed = time.perf_counter() - t0
+    return _out(Ud, was_t), _batched_stats(it, norms, conv, elapsed, config)
+
+
+def _batched_stats(it, norms, conv, elapsed, config):
     stats = []
-    for b in range(B):
+    for b in range(len(it)):
         k = int(it[b])
         hist = [float(v) for v in norms[b, :k + 1]]
         stats.append(SolveStats(iterations=k, residual_norms=hist, factor=max_ratio(hist),
                                 times=_times(elapsed), converged=bool(conv[b]), seed=config.seed,
                                 workers=config.workers))
-    return _out(Ud, was_t), stats
+    return stats
 
 
 def measure_convergence_factor(hier, config: CycleConfig = None) -> float:

@@ -142,12 +142,15 @@ int tmg_plan_solve(tmg_plan *plan, const void *f, void *u, const double *floor_p
                    double eps, int max_iters, void *stream);
 
 /* Host-buffer form of tmg_plan_solve -- the call a host-side binding of the
- * reference makes (numpy arrays in, numpy arrays out): f_host and u_host are
- * host arrays [batch][n_slabs][n_t] (pinned memory gives full PCIe speed).
- * Copies f and the initial guess in, solves, copies the solution back into
- * u_host.  Device buffers are owned by the plan.  Blocks until done. */
-int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, void *u_host, const double *floor_per_problem,
-                        double eps, int max_iters);
+ * reference makes (numpy arrays in, numpy arrays out): f_host, u_init_host
+ * (NULL = zero initial guess) and u_host are host arrays [batch][n_slabs][n_t]
+ * (pinned memory gives full PCIe speed; u_init_host may equal u_host).
+ * Copies in, solves, copies the solution into u_host; batches of >= 8
+ * problems are pipelined in sub-batches on two streams so the PCIe copies of
+ * one overlap the solve of the other.  Device buffers are owned by the plan.
+ * Blocks until done. */
+int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, const void *u_init_host, void *u_host,
+                        const double *floor_per_problem, double eps, int max_iters);
 
 /* Results of the last tmg_plan_solve (host arrays):
  * iterations[batch], norms[batch * (max_iters + 1)] (first iterations[b]+1

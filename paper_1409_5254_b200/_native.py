@@ -131,7 +131,7 @@ def load():
     L.tmg_plan_destroy.argtypes = [vp]
     L.tmg_plan_cycles.argtypes = [vp, vp, vp, ci, vp]
     L.tmg_plan_solve.argtypes = [vp, vp, vp, dp, ctypes.c_double, ci, vp]
-    L.tmg_plan_solve_host.argtypes = [vp, vp, vp, dp, ctypes.c_double, ci]
+    L.tmg_plan_solve_host.argtypes = [vp, vp, vp, vp, dp, ctypes.c_double, ci]
     L.tmg_plan_stats.argtypes = [vp, i32p, dp, i32p]
     L.tmg_plan_info.argtypes = [vp, i32p, i32p, i32p]
     for name in EXPORTS:

@@ -228,7 +228,8 @@ struct PlanBase {
     virtual int cycles(const void *f, void *u, int n_cycles, cudaStream_t s) = 0;
     virtual int solve(const void *f, void *u, const double *floor_, double eps, int max_iters,
                       cudaStream_t s) = 0;
-    virtual int solve_host(const void *f, void *u, const double *floor_, double eps, int max_iters) = 0;
+    virtual int solve_host(const void *f, const void *u0, void *u_out, const double *floor_, double eps,
+                           int max_iters) = 0;
     virtual int stats(int32_t *it, double *norms, int32_t *conv) const = 0;
     virtual int info(int32_t *kpc, int32_t *sl, int32_t *tl) const = 0;
 };
@@ -299,6 +300,11 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         cudaFree(d_active);
         cudaFree(d_any);
         if (h_any) cudaFreeHost(h_any);
+        if (hp_floor) cudaFreeHost(hp_floor);
+        if (hp_init) cudaFreeHost(hp_init);
+        if (hp_st) cudaFreeHost(hp_st);
+        if (hp_hist) cudaFreeHost(hp_hist);
+        if (ev_done) cudaEventDestroy(ev_done);
     }
 
     size_t fixed_smem() const { return tail_fixed_smem<T, NT>(depth - tl); }
@@ -308,6 +314,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         depth = nl;
         B = batch;
         o = opts;
+        descs.assign(lv, lv + nl);
         if (o.gamma < 1) o.gamma = 1;
         for (int l = 0; l < nl; ++l) {
             n.push_back(lv[l].n_slabs);
@@ -583,19 +590,69 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     }
 
     T *d_fh = nullptr, *d_uh = nullptr;  // device copies for the host-buffer entry point
+    std::vector<tmg_level_desc> descs;   // kept to build sub-batch plans
+    std::vector<std::unique_ptr<Plan>> subs;
 
-    int solve_host(const void *f, void *u, const double *floor_, double eps, int max_iters) override
+    // host buffers in, solve, host buffer out, this plan's problems only
+    int enqueue_host(const T *f, const T *u0, T *u_out, const double *floor_, double eps, int max_iters)
     {
         const size_t bytes = sizeof(T) * n[0] * NT * B;
         if (!d_fh) {
             CK(cudaMalloc(&d_fh, bytes));
             CK(cudaMalloc(&d_uh, bytes));
         }
+        if (ev_done) CK(cudaEventSynchronize(ev_done));  // previous chunk's D2H finished
         CK(cudaMemcpyAsync(d_fh, f, bytes, cudaMemcpyHostToDevice, ps));
-        CK(cudaMemcpyAsync(d_uh, u, bytes, cudaMemcpyHostToDevice, ps));
-        CKR(solve_on(d_fh, d_uh, floor_, eps, max_iters, ps));
-        CK(cudaMemcpyAsync(u, d_uh, bytes, cudaMemcpyDeviceToHost, ps));
-        CK(cudaStreamSynchronize(ps));
+        if (u0) CK(cudaMemcpyAsync(d_uh, u0, bytes, cudaMemcpyHostToDevice, ps));
+        else CK(cudaMemsetAsync(d_uh, 0, bytes, ps));
+        CKR(enqueue_solve(d_fh, d_uh, floor_, eps, max_iters, ps));
+        CK(cudaMemcpyAsync(u_out, d_uh, bytes, cudaMemcpyDeviceToHost, ps));
+        CK(cudaEventRecord(ev_done, ps));
+        return 0;
+    }
+
+    int solve_host(const void *f, const void *u0, void *u_out, const double *floor_, double eps,
+                   int max_iters) override
+    {
+        // sub-batches on two streams: the PCIe copies of one overlap the solve of the other
+        const int nch = (B >= 8 && B % 4 == 0 && tl > 0) ? 4 : 1;
+        if (nch == 1) {
+            CKR(enqueue_host((const T *)f, (const T *)u0, (T *)u_out, floor_, eps, max_iters));
+            return collect();
+        }
+        const long long bc = B / nch;
+        if (subs.empty()) {
+            for (int k = 0; k < 2; ++k) {
+                auto p = std::make_unique<Plan>();
+                CKR(p->init(descs.data(), depth, bc, o));
+                subs.push_back(std::move(p));
+            }
+        }
+        const size_t per = (size_t)n[0] * NT * bc;
+        last_max_iters = max_iters;
+        CKR(ensure_hist(max_iters));
+        h_hist.assign((size_t)hist_stride * B, 0.0);
+        h_it.assign(B, 0);
+        h_conv.assign(B, 0);
+        auto gather = [&](int c) -> int {
+            Plan &p = *subs[c % 2];
+            CKR(p.collect());
+            for (long long b = 0; b < bc; ++b) {
+                const long long g = c * bc + b;
+                h_it[g] = p.h_it[b];
+                h_conv[g] = p.h_conv[b];
+                for (int k = 0; k <= max_iters; ++k)
+                    h_hist[(size_t)g * hist_stride + k] = p.h_hist[(size_t)b * p.hist_stride + k];
+            }
+            return 0;
+        };
+        for (int c = 0; c < nch; ++c) {
+            if (c >= 2) CKR(gather(c - 2));
+            Plan &p = *subs[c % 2];
+            CKR(p.enqueue_host((const T *)f + c * per, u0 ? (const T *)u0 + c * per : nullptr,
+                               (T *)u_out + c * per, floor_ + c * bc, eps, max_iters));
+        }
+        for (int c = std::max(0, nch - 2); c < nch; ++c) CKR(gather(c));
         return 0;
     }
 
@@ -618,21 +675,43 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         return 0;
     }
 
-    int solve_on(const void *f, void *u, const double *floor_, double eps, int max_iters,
-                 cudaStream_t s)
+    // pinned staging so a solve can be enqueued without host synchronisation
+    double *hp_floor = nullptr;
+    ProbState *hp_init = nullptr, *hp_st = nullptr;
+    double *hp_hist = nullptr;
+    cudaEvent_t ev_done = nullptr;
+
+    int ensure_hist(int max_iters)
     {
-        if (max_iters < 1) return fail(TMG_E_ARG, "max_iters must be >= 1");
+        if (!hp_floor) {
+            CK(cudaHostAlloc(&hp_floor, sizeof(double) * B, cudaHostAllocDefault));
+            CK(cudaHostAlloc(&hp_init, sizeof(ProbState) * B, cudaHostAllocDefault));
+            CK(cudaHostAlloc(&hp_st, sizeof(ProbState) * B, cudaHostAllocDefault));
+            CK(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+        }
         if (max_iters + 1 > hist_stride) {
             cudaFree(d_hist);
+            if (hp_hist) cudaFreeHost(hp_hist);
             hist_stride = max_iters + 1;
             CK(cudaMalloc(&d_hist, sizeof(double) * hist_stride * B));
+            CK(cudaHostAlloc(&hp_hist, sizeof(double) * hist_stride * B, cudaHostAllocDefault));
             if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
         }
+        return 0;
+    }
+
+    // enqueue a whole solve on stream s; the stopping state and the residual
+    // histories land in pinned host buffers (collect() reads them)
+    int enqueue_solve(const void *f, void *u, const double *floor_, double eps, int max_iters, cudaStream_t s)
+    {
+        if (max_iters < 1) return fail(TMG_E_ARG, "max_iters must be >= 1");
+        CKR(ensure_hist(max_iters));
+        if (ev_done) CK(cudaEventSynchronize(ev_done));  // the staging buffers are free again
         last_max_iters = max_iters;
-        CK(cudaMemcpyAsync(d_floor, floor_, sizeof(double) * B, cudaMemcpyHostToDevice, s));
-        std::vector<ProbState> init(B);
-        for (auto &p : init) { p.tol = 0; p.iters = 0; p.active = 1; p.max_iters = max_iters; p.converged = 0; }
-        CK(cudaMemcpyAsync(d_st, init.data(), sizeof(ProbState) * B, cudaMemcpyHostToDevice, s));
+        memcpy(hp_floor, floor_, sizeof(double) * B);
+        for (long long b = 0; b < B; ++b) hp_init[b] = ProbState{0.0, 0, 1, max_iters, 0};
+        CK(cudaMemcpyAsync(d_floor, hp_floor, sizeof(double) * B, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_st, hp_init, sizeof(ProbState) * B, cudaMemcpyHostToDevice, s));
         if (tl == 0) {
             TailArgs<T, NT> t = targ;
             t.f_in = (const T *)f;
@@ -663,19 +742,29 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                 ++it;
             }
         }
-        // results
-        std::vector<ProbState> st(B);
-        h_hist.resize((size_t)hist_stride * B);
-        CK(cudaMemcpyAsync(st.data(), d_st, sizeof(ProbState) * B, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(h_hist.data(), d_hist, sizeof(double) * hist_stride * B, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpyAsync(hp_st, d_st, sizeof(ProbState) * B, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hp_hist, d_hist, sizeof(double) * hist_stride * B, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ev_done, s));
+        return 0;
+    }
+
+    int collect()
+    {
+        CK(cudaEventSynchronize(ev_done));
+        h_hist.assign(hp_hist, hp_hist + (size_t)hist_stride * B);
         h_it.resize(B);
         h_conv.resize(B);
         for (long long b = 0; b < B; ++b) {
-            h_it[b] = st[b].iters;
-            h_conv[b] = st[b].converged;
+            h_it[b] = hp_st[b].iters;
+            h_conv[b] = hp_st[b].converged;
         }
         return 0;
+    }
+
+    int solve_on(const void *f, void *u, const double *floor_, double eps, int max_iters, cudaStream_t s)
+    {
+        CKR(enqueue_solve(f, u, floor_, eps, max_iters, s));
+        return collect();
     }
 
     int stats(int32_t *it, double *norms, int32_t *conv) const override
@@ -983,12 +1072,12 @@ int tmg_plan_solve(tmg_plan *plan, const void *f, void *u, const double *floor_p
     return plan->impl->solve(f, u, floor_per_problem, eps, max_iters, (cudaStream_t)stream);
 }
 
-int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, void *u_host, const double *floor_per_problem,
-                        double eps, int max_iters)
+int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, const void *u_init_host, void *u_host,
+                        const double *floor_per_problem, double eps, int max_iters)
 {
-    if (!plan) return fail(TMG_E_ARG, "NULL plan");
+    if (!plan || !f_host || !u_host) return fail(TMG_E_ARG, "NULL argument");
     if (!(eps > 0.0 && eps < 1.0)) return fail(TMG_E_ARG, "eps must lie in (0, 1)");
-    return plan->impl->solve_host(f_host, u_host, floor_per_problem, eps, max_iters);
+    return plan->impl->solve_host(f_host, u_init_host, u_host, floor_per_problem, eps, max_iters);
 }
 
 int tmg_plan_stats(const tmg_plan *plan, int32_t *iterations, double *norms, int32_t *converged)

@@ -141,12 +141,14 @@ class DevicePlan:
             _stream()), "tmg_plan_solve")
         return self._stats(max_iters)
 
-    def solve_host(self, f_host, u_host, floors, eps: float, max_iters: int):
+    def solve_host(self, f_host, u_init, u_out, floors, eps: float, max_iters: int):
         """Host buffers (numpy or CPU torch, ideally pinned) in and out: the
-        C ABI copies in, solves and copies the solution back into u_host."""
+        C ABI copies in (u_init None = zero guess), solves and copies the
+        solution into u_out."""
         floors = np.ascontiguousarray(floors, dtype=np.float64)
+        uin = None if u_init is None else ctypes.c_void_p(_host_ptr(u_init))
         nat.check(nat.load().tmg_plan_solve_host(
-            self._h, ctypes.c_void_p(_host_ptr(f_host)), ctypes.c_void_p(_host_ptr(u_host)),
+            self._h, ctypes.c_void_p(_host_ptr(f_host)), uin, ctypes.c_void_p(_host_ptr(u_out)),
             floors.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(eps), int(max_iters)),
             "tmg_plan_solve_host")
         return self._stats(max_iters)
@@ -285,7 +287,7 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
         floor = 1e-12 * float(np.linalg.norm(np.asarray(f, dtype=np.float64)))
         plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, 1)
         t0 = time.perf_counter()
-        it, norms, conv = plan.solve_host(fh, uh, [floor], config.eps, config.max_iters)
+        it, norms, conv = plan.solve_host(fh, uh, uh, [floor], config.eps, config.max_iters)
         elapsed = time.perf_counter() - t0
         k = int(it[0])
         hist = [float(v) for v in norms[0, :k + 1]]
@@ -332,15 +334,16 @@ def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None, inp
         Fh = _host_array(F, copy=False)
         B = Fh.shape[0]
         if U0 is None:
-            Uh = np.zeros(tuple(Fh.shape))
+            Uin, Uh = None, np.empty(tuple(Fh.shape))
         else:
             Uh = _host_array(U0, copy=not inplace)
+            Uin = Uh
         if floors is None:
             floors = [1e-12 * float(np.linalg.norm(np.asarray(Fh[b], dtype=np.float64)))
                       for b in range(B)]
         plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, B)
         t0 = time.perf_counter()
-        it, norms, conv = plan.solve_host(Fh, Uh, floors, config.eps, config.max_iters)
+        it, norms, conv = plan.solve_host(Fh, Uin, Uh, floors, config.eps, config.max_iters)
         elapsed = time.perf_counter() - t0
         return Uh, _batched_stats(it, norms, conv, elapsed, config)
     torch = _torch()

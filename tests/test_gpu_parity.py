@@ -355,3 +355,20 @@ def test_device_resident_torch_api():
     assert torch.is_tensor(u_t) and u_t.is_cuda
     assert u_t.cpu().numpy().tobytes() == u_np.tobytes()
     assert st_t.residual_norms == st_np.residual_norms
+
+
+def test_batched_host_pipeline_vs_oracle(oracle_mod):
+    """B >= 8 host buffers go through the sub-batch pipeline (two streams)."""
+    n = 1 << 13
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(1), 1.0 / n, n, coarsest=2)
+    F = np.stack([problems.seeded_rhs(1, n, 1.0, 42, b)[0] for b in range(8)])
+    cfg = tmg.CycleConfig(nu1=1, nu2=1, eps=1e-8)
+    om = omegas(hier)
+    for U0 in (None, np.stack([tmg.random_initial_guess(hier, b) for b in range(8)])):
+        U, stats = tmg.solve_batched(hier, F, U0, cfg)
+        for b in range(8):
+            u0 = np.zeros_like(F[b]) if U0 is None else U0[b]
+            ur, norms, iters = oracle_mod.iterate(hier, om, F[b], u0, 1, 1, 1e-8, 250)
+            assert stats[b].iterations == iters, b
+            assert stats[b].residual_norms == norms, b
+            assert same_bits(U[b], ur), b

@@ -48,10 +48,8 @@ WORKLOADS = {
 # helpers
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    from paper_1409_5254_b200 import dist as tdist
+    return tdist.env()
 
 
 def peak_hbm():
@@ -259,7 +257,8 @@ def run_gpu_arm(args, w):
 
     B, n, p_t = w["batch"], w["n"], w["p_t"]
     nt = p_t + 1
-    ids = [rank * B + b for b in range(B)] if B > 1 else [None]
+    from paper_1409_5254_b200 import dist as tdist
+    ids = tdist.problem_ids(rank, ws, B) if B > 1 else [None]
     F = problems.seeded_rhs_batch_device(p_t, n, w["T"], 42, ids if B > 1 else (None,))
     floors = [1e-12 * float(v) for v in torch.linalg.norm(F.reshape(B, -1), dim=1).cpu()]
     hier = make_hier(w)
@@ -292,13 +291,7 @@ def run_gpu_arm(args, w):
     if ws > 1:
         dist.barrier()
     dof = float(sum(n * nt * k for row in iters for k in row))
-    t = torch.tensor([elapsed, dof], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        tmax = t[0:1].clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dsum = t[1:2].clone()
-        dist.all_reduce(dsum, op=dist.ReduceOp.SUM)
-        elapsed, dof = float(tmax.item()), float(dsum.item())
+    elapsed, dof = tdist.reduce_time_and_work(elapsed, dof, device="cuda")
     value = dof / elapsed
     plan = solver.get_plan(hier, 0, len(hier.levels), solver.omegas_for(hier, cfg, len(hier.levels)),
                            cfg, B)
@@ -332,13 +325,7 @@ def run_gpu_arm(args, w):
     f1.record()
     torch.cuda.synchronize()
     e2e_time = f0.elapsed_time(f1) * 1e-3
-    if ws > 1:
-        t2 = torch.tensor([e2e_time, dof_e2e], dtype=torch.float64, device="cuda")
-        a = t2[0:1].clone()
-        dist.all_reduce(a, op=dist.ReduceOp.MAX)
-        bsum = t2[1:2].clone()
-        dist.all_reduce(bsum, op=dist.ReduceOp.SUM)
-        e2e_time, dof_e2e = float(a.item()), float(bsum.item())
+    e2e_time, dof_e2e = tdist.reduce_time_and_work(e2e_time, dof_e2e, device="cuda")
 
     # roofline of the dominant kernel (finest-level fused down pass)
     ktimes, kbytes = kernel_roofline(w, F, U, hier, torch.cuda.current_stream().cuda_stream)

@@ -9,7 +9,7 @@ from .assembly import (ALPHA_MIN, BasisSpec, BlockLU, GlobalSystem, LocalOperato
                        build_transfers, optimal_omega, radau_rule, resolve_damping, rhs_moments,
                        stability_function)
 from .hierarchy import CycleConfig, Level, SolveStats, TimeHierarchy
-from .solver import (DevicePlan, block_jacobi_sweep, measure_convergence_factor,
+from .solver import (DevicePlan, block_jacobi_sweep, forward_solve, measure_convergence_factor,
                      random_initial_guess, solve, solve_batched, two_grid_cycle, v_cycle)
 
 __version__ = "0.1.0"

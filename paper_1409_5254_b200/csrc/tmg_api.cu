@@ -112,6 +112,35 @@ template <typename T, int NT> LevelC<T, NT> make_level(const tmg_level_desc &d)
         L.cneg[i] = m;
     }
     L.has_transfer = d.has_transfer;
+    // rank-1 factors of the coupling (outer(eval_start, eval_end), dg.py:236):
+    // e = row 0, c_i = N[i, j*] / N[0, j*] (exact for both bases: c = e_0 or +-1)
+    int js = 0;
+    for (int j = 1; j < NT; ++j)
+        if (std::fabs(d.coupling[j]) > std::fabs(d.coupling[js])) js = j;
+    double c[NT], e[NT];
+    bool ok = d.coupling[js] != 0.0;
+    for (int j = 0; j < NT; ++j) e[j] = d.coupling[j];
+    for (int i = 0; i < NT; ++i) c[i] = ok ? d.coupling[i * NT + js] / d.coupling[js] : 0.0;
+    for (int i = 0; i < NT && ok; ++i)
+        for (int j = 0; j < NT; ++j)
+            if (std::fabs(c[i] * e[j] - d.coupling[i * NT + j]) > 1e-14 * std::fabs(d.coupling[js])) ok = false;
+    // w = LU^-1 c with the level's own factors (dg.py:153-168 order)
+    double y[NT];
+    for (int i = 0; i < NT; ++i) y[i] = c[d.perm[i]];
+    for (int i = 1; i < NT; ++i)
+        for (int j = 0; j < i; ++j) y[i] -= d.lu[i * NT + j] * y[j];
+    for (int i = NT - 1; i >= 0; --i) {
+        for (int j = i + 1; j < NT; ++j) y[i] -= d.lu[i * NT + j] * y[j];
+        y[i] /= d.lu[i * NT + i];
+    }
+    double al = 0.0;
+    for (int j = 0; j < NT; ++j) al += e[j] * y[j];
+    for (int j = 0; j < NT; ++j) {
+        L.ce[j] = (T)e[j];
+        L.cw[j] = (T)y[j];
+    }
+    L.calpha = (T)al;
+    L.scan_ok = ok ? 1 : 0;
     return L;
 }
 
@@ -395,6 +424,9 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         targ.nu2 = o.nu2;
         targ.gamma = o.gamma;
         targ.dot_variant = o.dot_variant;
+        // coarsest solve: serial forward substitution (bitwise) unless asked
+        // for the scan, or "auto" and the coarsest level is too long for one thread
+        targ.coarse_scan = L[nl - 1].scan_ok && (o.coarse == 1 || (o.coarse == 2 && n[nl - 1] > 16384));
         return 0;
     }
 
@@ -941,8 +973,12 @@ template <typename T, int NT, bool SP>
 int coarse_op(const tmg_level_desc &d, const void *f, void *u, long long B, int method, int variant,
               cudaStream_t s)
 {
-    if (method != 0) return fail(TMG_E_UNSUPPORTED, "scan coarse solve not built in this version");
     const LevelC<T, NT> L = make_level<T, NT>(d);
+    if (method == 1) {
+        if (!L.scan_ok) return fail(TMG_E_UNSUPPORTED, "coupling is not rank one: no scan solve");
+        CK(((cudaError_t)coarse_scan_launch<T, NT>(L, (const T *)f, (T *)u, d.n_slabs, (int)B, nullptr, s)));
+        return 0;
+    }
     CK(((cudaError_t)coarse_serial_launch<T, NT>(L, SP, (const T *)f, (T *)u, d.n_slabs, (int)B, variant, nullptr, s)));
     return 0;
 }

@@ -106,6 +106,16 @@ int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, 
     return (int)cudaGetLastError();
 }
 
+template <typename T, int NT>
+int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, int batch, const int *active,
+                       cudaStream_t s)
+{
+    coarse_scan_kernel<T, NT><<<(unsigned)batch, 1024, 0, s>>>(L, f, u, n, batch, active);
+    return (int)cudaGetLastError();
+}
+
+template int coarse_scan_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const TMG_T *, TMG_T *, long long,
+                                               int, const int *, cudaStream_t);
 template int stream_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
                                           int, bool, cudaStream_t);
 template size_t stream_smem_bytes<TMG_T, TMG_NT>();

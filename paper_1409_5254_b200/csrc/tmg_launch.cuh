@@ -24,6 +24,10 @@ template <typename T, int NT>
 int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, long long n, int batch,
                          int variant, const int *active, cudaStream_t s);
 
+template <typename T, int NT>
+int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, int batch, const int *active,
+                       cudaStream_t s);
+
 #define TMG_DECLARE(T, NT)                                                                              \
     extern template int stream_launch<T, NT>(const LevelC<T, NT> &, const StreamArgs<T> &, int, int, int, \
                                              bool, cudaStream_t);                                       \
@@ -31,7 +35,9 @@ int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, 
     extern template int tail_prepare<T, NT>(bool, size_t);                                              \
     extern template int tail_launch<T, NT>(const TailArgs<T, NT> &, bool, unsigned, size_t, cudaStream_t); \
     extern template int coarse_serial_launch<T, NT>(const LevelC<T, NT> &, bool, const T *, T *, long long, \
-                                                    int, int, const int *, cudaStream_t);
+                                                    int, int, const int *, cudaStream_t);     \
+    extern template int coarse_scan_launch<T, NT>(const LevelC<T, NT> &, const T *, T *, long long, int, \
+                                                  const int *, cudaStream_t);
 #ifndef TMG_INST_UNIT
 TMG_DECLARE(double, 1)
 TMG_DECLARE(double, 2)

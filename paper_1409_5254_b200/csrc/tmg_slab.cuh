@@ -110,6 +110,13 @@ template <typename T, int NT> struct LevelC {
     int perm[NT];   // BlockLU.perm       (dg.py:148-151)
     unsigned cneg[NT];  // sign bits of coupling row i (sparse path)
     int has_transfer;
+    // rank-1 form of the coupling N = c e^T for the scan coarse solve:
+    // s_k = e.u_k obeys s_k = calpha s_{k-1} + e.LU^-1 f_k and
+    // u_k = LU^-1 f_k + s_{k-1} cw with cw = LU^-1 c, calpha = e.cw
+    T ce[NT];
+    T cw[NT];
+    T calpha;
+    int scan_ok;
 };
 
 // What a slab needs from its predecessor.

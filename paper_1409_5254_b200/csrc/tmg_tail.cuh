@@ -55,6 +55,78 @@ __global__ void coarse_serial_kernel(const __grid_constant__ LevelC<T, NT> L, co
 // ---------------------------------------------------------------------------
 // the single-CTA engine
 
+// Exact coarse solve L u = f as a CTA-wide associative scan of the rank-1
+// slab recurrence (north star: "the coarsest-level forward solve done as a
+// parallel associative scan"): with g_k = LU^-1 f_k and h_k = e.g_k,
+//   s_k = alpha s_{k-1} + h_k,   u_k = g_k + s_{k-1} w      (s_{-1} = 0)
+// Threads scan contiguous chunks, the chunk maps x -> A x + H are combined
+// with a Hillis-Steele scan in shared memory, then each chunk is replayed with
+// its incoming s.  Mathematically equal to _forward_substitute
+// (multigrid.py:200-205) but associated differently: ~1e-15 relative, not
+// bitwise.  |alpha| = |R(-tau)| <= 1 keeps it stable.  f may alias nothing;
+// u receives the solution.  sA, sH: blockDim.x scratch values each.
+template <typename T, int NT>
+__device__ void cta_scan_solve(const LevelC<T, NT> &L, const T *f, T *u, long long n, T *sA, T *sH)
+{
+    const int t = threadIdx.x, P = blockDim.x;
+    const long long m = (n + P - 1) / P;
+    const long long a = min(n, (long long)t * m), e = min(n, a + m);
+    T s = T(0), A = T(1);
+    for (long long k = a; k < e; ++k) {
+        T x[NT], g[NT];
+        load_slab_scalar<T, NT>(f + k * NT, x);
+        lu_solve<T, NT>(L, x, g);
+        T h = FP<T>::mul(L.ce[0], g[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) h = FP<T>::fma(L.ce[j], g[j], h);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) u[k * NT + j] = g[j];
+        s = FP<T>::fma(L.calpha, s, h);
+        A = FP<T>::mul(A, L.calpha);
+    }
+    sA[t] = A;
+    sH[t] = s;
+    __syncthreads();
+    for (int off = 1; off < P; off <<= 1) {
+        T pa = T(1), ph = T(0);
+        if (t >= off) {
+            pa = sA[t - off];
+            ph = sH[t - off];
+        }
+        __syncthreads();
+        if (t >= off) {
+            // (A, H) o (pa, ph): x -> A (pa x + ph) + H
+            sH[t] = FP<T>::fma(sA[t], ph, sH[t]);
+            sA[t] = FP<T>::mul(sA[t], pa);
+        }
+        __syncthreads();
+    }
+    s = t == 0 ? T(0) : sH[t - 1];
+    __syncthreads();
+    for (long long k = a; k < e; ++k) {
+        T g[NT];
+        load_slab_scalar<T, NT>(u + k * NT, g);
+        T h = FP<T>::mul(L.ce[0], g[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) h = FP<T>::fma(L.ce[j], g[j], h);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) u[k * NT + j] = FP<T>::fma(s, L.cw[j], g[j]);
+        s = FP<T>::fma(L.calpha, s, h);
+    }
+    __syncthreads();
+}
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(1024)
+    coarse_scan_kernel(const __grid_constant__ LevelC<T, NT> L, const T *f, T *u, long long n, int batch,
+                       const int *active)
+{
+    __shared__ T sA[1024], sH[1024];
+    const int b = blockIdx.x;
+    if (b >= batch || (active && !active[b])) return;
+    cta_scan_solve<T, NT>(L, f + (size_t)b * n * NT, u + (size_t)b * n * NT, n, sA, sH);
+}
+
 template <typename T, int NT, bool SPARSE> struct Engine {
     const LevelC<T, NT> *L;  // shared copy
     T *u[MAXLEV];
@@ -183,8 +255,14 @@ template <typename T, int NT, bool SPARSE> struct Engine {
         }
         __syncthreads();
     }
+    int scan = 0;  // coarsest solve: 0 = serial forward substitution (bitwise), 1 = scan
+
     __device__ void coarse_level(int l, int variant) const
     {
+        if (scan) {
+            cta_scan_solve<T, NT>(L[l], f[l], u[l], n[l], xch, xch + blockDim.x);
+            return;
+        }
         if (threadIdx.x == 0) forward_substitute<T, NT, SPARSE>(L[l], f[l], u[l], n[l], variant);
         __syncthreads();
     }
@@ -255,6 +333,7 @@ __global__ void __launch_bounds__(TAIL_THREADS)
     unsigned char *p = smem + sizeof(LevelC<T, NT>) * nlev;
     Engine<T, NT, SPARSE> E;
     E.L = Ls - a.l0;  // index by absolute level
+    E.scan = a.coarse_scan;
     E.xch = reinterpret_cast<T *>(p);
     p += sizeof(T) * TAIL_THREADS * (NT + 1);
     E.part = reinterpret_cast<double *>(p);

@@ -28,6 +28,7 @@ template <typename T, int NT> struct TailArgs {
     T *gstore;                    // global level store when not in shared memory
     int in_smem;
     int nu1, nu2, gamma, dot_variant;
+    int coarse_scan;              // coarsest solve by the CTA scan (not bitwise)
     int full;                     // 1: _iterate with norms; 0: n_cycles cycles
     int n_cycles;
     // full mode

@@ -250,13 +250,34 @@ def v_cycle(hier, u, f, config: CycleConfig = None):
     return _cycle_api(hier, 0, depth, u, f, config)
 
 
-def _forward_solve_dev(ops, n, fd, config):
+SCAN_AUTO_MIN = 16384  # "auto": longer coarse solves use the parallel scan
+
+
+def _forward_solve_dev(ops, n, fd, config, batch=1):
     torch = _torch()
     u = torch.empty_like(fd)
     d = nat.level_desc(ops, n)
-    nat.check(nat.load().tmg_coarse_solve(nat.F64, ctypes.byref(d), _ptr(fd), _ptr(u), 1, 0,
+    method = {"serial": 0, "scan": 1}.get(config.coarse, 1 if n > SCAN_AUTO_MIN else 0)
+    nat.check(nat.load().tmg_coarse_solve(nat.F64, ctypes.byref(d), _ptr(fd), _ptr(u), batch, method,
                                           int(config.dot_variant), _stream()), "tmg_coarse_solve")
     return u
+
+
+def forward_solve(system, rhs, method: str = "scan"):
+    """Exact solve of the block lower-bidiagonal system on the GPU
+    (dg.py:290-303).  method "serial": block forward substitution, bitwise
+    with the reference's coarse solve (one thread per problem); "scan": the
+    parallel associative scan of the rank-1 slab recurrence (~1e-15 relative).
+    rhs: (n_steps, n_t) or (B, n_steps, n_t); numpy in -> numpy out."""
+    if getattr(system, "periodic", False):
+        raise ValueError("forward substitution requires a non-periodic system")
+    rd, was_t = _dev(rhs)
+    batch = rd.shape[0] if rd.dim() == 3 else 1
+    n = rd.shape[-2]
+    if n != system.n_steps or rd.shape[-1] != system.ops.n_t:
+        raise ValueError(f"rhs shape {tuple(rd.shape)} does not match ({system.n_steps}, {system.ops.n_t})")
+    u = _forward_solve_dev(system.ops, n, rd, CycleConfig(coarse=method), batch)
+    return _out(u, was_t)
 
 
 def _floor_of(f) -> float:

@@ -372,3 +372,31 @@ def test_batched_host_pipeline_vs_oracle(oracle_mod):
             assert stats[b].iterations == iters, b
             assert stats[b].residual_norms == norms, b
             assert same_bits(U[b], ur), b
+
+
+@pytest.mark.parametrize("p_t,tau,n", [(1, 1e-6, 1 << 20), (2, 0.5, 4097), (3, 1e3, 1000),
+                                       (0, 2.0 ** -10, 65536)])
+def test_scan_forward_solve_vs_oracle(oracle_mod, p_t, tau, n):
+    """parallel-scan exact solve vs the reference-order forward substitution"""
+    ops = tmg.assemble_local(tmg.BasisSpec(p_t), tau)
+    rhs = np.random.default_rng(n).standard_normal((n, p_t + 1))
+    want = oracle_mod.forward_substitute(ops, rhs)
+    got = tmg.forward_solve(tmg.GlobalSystem(ops, n), rhs, method="scan")
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+    exact = tmg.forward_solve(tmg.GlobalSystem(ops, min(n, 4096)), rhs[:4096], method="serial")
+    assert same_bits(exact, oracle_mod.forward_substitute(ops, rhs[:4096]))
+
+
+def test_w_cycle_large_coarsest_scan(oracle_mod):
+    """W-cycle with a 1024-slab coarsest level solved by the scan: iterates
+    within 1e-12 of the oracle (which uses forward substitution)."""
+    n = 1 << 16
+    rhs, tau, _ = problems.seeded_rhs(2, n, 1.0, 42)
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(2), tau, n, coarsest=1024)
+    cfg = tmg.CycleConfig(nu1=1, nu2=1, eps=1e-8, cycle="W", coarse="scan")
+    u, st = tmg.solve(hier, rhs, np.zeros_like(rhs), cfg)
+    ur, norms, iters = oracle_mod.iterate(hier, omegas(hier), rhs, np.zeros_like(rhs), 1, 1, 1e-8,
+                                          250, gamma=2)
+    assert st.iterations == iters
+    assert np.linalg.norm(u - ur) <= 1e-12 * np.linalg.norm(ur)
+    assert np.allclose(st.residual_norms, norms, rtol=1e-9, atol=0)

@@ -382,7 +382,10 @@ def test_scan_forward_solve_vs_oracle(oracle_mod, p_t, tau, n):
     rhs = np.random.default_rng(n).standard_normal((n, p_t + 1))
     want = oracle_mod.forward_substitute(ops, rhs)
     got = tmg.forward_solve(tmg.GlobalSystem(ops, n), rhs, method="scan")
-    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+    # both orders carry O(n eps) rounding through the recurrence (|alpha| ~ 1
+    # for small steps); the scan may not differ from the serial sweep by more
+    tol = max(1e-12, 4e-16 * n)
+    assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want)
     exact = tmg.forward_solve(tmg.GlobalSystem(ops, min(n, 4096)), rhs[:4096], method="serial")
     assert same_bits(exact, oracle_mod.forward_substitute(ops, rhs[:4096]))
 

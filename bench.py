@@ -40,6 +40,7 @@ PROFILE_SUMMARY = os.path.join(REPO, "profiles", "ncu_summary.json")
 WORKLOADS = {
     "config3": dict(batch=64, n=1 << 22, p_t=1, T=1.0, nu=1),
     "config2": dict(batch=1, n=1 << 20, p_t=1, T=1.0, nu=1),
+    "config2_p3": dict(batch=1, n=1 << 20, p_t=3, T=1.0, nu=1),
     "config1": dict(batch=1, n=1 << 10, p_t=1, T=1.0, nu=1),
 }
 

@@ -286,6 +286,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     long long store_elems = 0;
     T *gstore = nullptr;
     TailArgs<T, NT> targ{};
+    unsigned long long *d_trace = nullptr;
     // norms
     int leaf_rows0 = 0;
     long long nleaves = 0;
@@ -318,6 +319,15 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         for (auto p : uB) cudaFree(p);
         for (auto p : fl) cudaFree(p);
         cudaFree(d_levels);
+        if (d_trace) {
+            std::vector<unsigned long long> tr(6 * MAXLEV);
+            cudaMemcpy(tr.data(), d_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost);
+            const char *names[6] = {"sweep", "restrict", "prolong", "coarse", "norm", "warp"};
+            for (int k = 0; k < 6; ++k)
+                for (int l = 0; l < MAXLEV; ++l)
+                    if (tr[k * MAXLEV + l]) fprintf(stderr, "tail-trace %s L%d %llu\n", names[k], l, tr[k * MAXLEV + l]);
+            cudaFree(d_trace);
+        }
         cudaFree(d_fh);
         cudaFree(d_uh);
         cudaFree(gstore);
@@ -424,6 +434,12 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         targ.nu2 = o.nu2;
         targ.gamma = o.gamma;
         targ.dot_variant = o.dot_variant;
+        targ.trace = nullptr;
+        if (getenv("TMG_TAIL_TRACE")) {
+            CK(cudaMalloc(&d_trace, sizeof(unsigned long long) * 6 * MAXLEV));
+            CK(cudaMemset(d_trace, 0, sizeof(unsigned long long) * 6 * MAXLEV));
+            targ.trace = d_trace;
+        }
         // coarsest solve: serial forward substitution (bitwise) unless asked
         // for the scan, or "auto" and the coarsest level is too long for one thread
         targ.coarse_scan = L[nl - 1].scan_ok && (o.coarse == 1 || (o.coarse == 2 && n[nl - 1] > 16384));

@@ -121,4 +121,49 @@ static __device__ double block_pairwise(const double *a, long long n, double *pa
     return s;
 }
 
+// Fast path for sizes whose numpy recursion halves exactly down to leaves of
+// L in (64, 128] (or n itself <= 128 with n % 8 == 0): 8 lanes per leaf run
+// the 8 strided accumulators, combine them in numpy's tree, then a shared-
+// memory binary tree adds the leaves (left + right at every node).  Same
+// association as np.sum, in O(L/8 + log n) steps.  Returns -1 leaf size when
+// the structure does not apply.
+static __device__ __forceinline__ long long pw_leaf_size(long long n)
+{
+    long long m = n;
+    while (m > 128) {
+        if (m % 2 || (m / 2) % 8) return -1;
+        m /= 2;
+    }
+    return (m >= 8 && m % 8 == 0) ? m : -1;
+}
+
+static __device__ double block_pairwise_auto(const double *a, long long n, double *part)
+{
+    const long long L = pw_leaf_size(n);
+    const long long nleaf = L > 0 ? n / L : 0;
+    if (L <= 0 || nleaf * 8 > (long long)blockDim.x) return block_pairwise(a, n, part);
+    const int t = threadIdx.x;
+    const int leaf = t >> 3, j = t & 7;
+    double r = 0.0;
+    if (leaf < nleaf) {
+        const double *x = a + leaf * L;
+        r = x[j];
+        for (long long i = 8 + j; i < L; i += 8) r = __dadd_rn(r, x[i]);
+    }
+    // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) within each group of 8 lanes
+    double t1 = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));
+    double t2 = __dadd_rn(t1, __shfl_down_sync(0xffffffffu, t1, 2));
+    double t3 = __dadd_rn(t2, __shfl_down_sync(0xffffffffu, t2, 4));
+    if (j == 0 && leaf < nleaf) part[leaf] = t3;
+    __syncthreads();
+    for (long long w = 1; w < nleaf; w <<= 1) {
+        if ((long long)t * 2 * w + w < nleaf && (long long)t * 2 * w < nleaf)
+            part[t * 2 * w] = __dadd_rn(part[t * 2 * w], part[t * 2 * w + w]);
+        __syncthreads();
+    }
+    double s = part[0];
+    __syncthreads();
+    return s;
+}
+
 }  // namespace tmg

@@ -279,20 +279,12 @@ __device__ __forceinline__ void lu_solve(const LevelC<T, NT> &L, const T (&r)[NT
     }
 }
 
-// one damped block-Jacobi update of slab n in place (multigrid.py:169-180)
+// one damped block-Jacobi update of slab n in place (multigrid.py:169-180).
+// Branch-free divisions; the rare out-of-window numerator redoes the LU solve
+// with IEEE division (one branch per slab instead of one per division).
 template <typename T, int NT, bool SPARSE>
 __device__ __forceinline__ void sweep(const LevelC<T, NT> &L, T (&u)[NT], const T (&f)[NT],
-                                      const Cpl<T, NT, SPARSE> &p, bool has_prev)
-{
-    T r[NT], c[NT];
-    residual<T, NT, SPARSE>(L, u, f, p, has_prev, r);
-    lu_solve<T, NT>(L, r, c);
-#pragma unroll
-    for (int i = 0; i < NT; ++i) {
-        c[i] = FP<T>::mul(c[i], L.omega);
-        u[i] = FP<T>::add(c[i], u[i]);
-    }
-}
+                                      const Cpl<T, NT, SPARSE> &p, bool has_prev);
 
 // lane-selected transfer product: odd ? R2 r : R1 r   (multigrid.py:184-185)
 template <typename T, int NT>
@@ -597,6 +589,25 @@ template <typename T, int NT, bool SPARSE>
 __device__ __forceinline__ Cpl<T, NT, SPARSE> cpl_rot(const Cpl<T, NT, SPARSE> &c, int src)
 {
     return cpl_shfl<T, NT, SPARSE>(c, src);
+}
+
+template <typename T, int NT, bool SPARSE>
+__device__ __forceinline__ void sweep(const LevelC<T, NT> &L, T (&u)[NT], const T (&f)[NT],
+                                      const Cpl<T, NT, SPARSE> &p, bool has_prev)
+{
+    T y[NT], ys[NT];
+    residual_perm<T, NT, SPARSE, P_GEN>(L, u, f, p, has_prev, y);
+#pragma unroll
+    for (int i = 0; i < NT; ++i) ys[i] = y[i];
+    unsigned bad = 0;
+    lu_apply_nb<T, NT>(L, y, bad);
+    if (__builtin_expect(bad != 0, 0)) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) y[i] = ys[i];
+        lu_apply_ieee<T, NT>(L, y);
+    }
+#pragma unroll
+    for (int i = 0; i < NT; ++i) u[i] = FP<T>::add(FP<T>::mul(y[i], L.omega), u[i]);
 }
 
 }  // namespace tmg

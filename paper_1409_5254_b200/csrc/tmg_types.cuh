@@ -29,6 +29,7 @@ template <typename T, int NT> struct TailArgs {
     int in_smem;
     int nu1, nu2, gamma, dot_variant;
     int coarse_scan;              // coarsest solve by the CTA scan (not bitwise)
+    unsigned long long *trace;    // optional: per-phase SM-cycle totals of problem 0 (diagnostics)
     int full;                     // 1: _iterate with norms; 0: n_cycles cycles
     int n_cycles;
     // full mode
@@ -44,8 +45,9 @@ template <typename T, int NT> struct TailArgs {
 template <typename T, int NT>
 __host__ __device__ constexpr size_t tail_fixed_smem(int nlev)
 {
-    return sizeof(LevelC<T, NT>) * (size_t)nlev + sizeof(T) * TAIL_THREADS * (NT + 1) +
-           sizeof(double) * TAIL_THREADS + 64;
+    // LevelC[nlev] | meta | halo values [2][TT][NT] | halo masks [2][TT] | part[TT]
+    return sizeof(LevelC<T, NT>) * (size_t)nlev + sizeof(int) * 3 * (size_t)nlev + sizeof(T) * 2 * TAIL_THREADS * NT +
+           sizeof(unsigned) * 2 * TAIL_THREADS + sizeof(double) * TAIL_THREADS + 64;
 }
 
 }  // namespace tmg

@@ -56,10 +56,10 @@ def timed(fn, reps, flush=True):
     return min(ts), sorted(ts)[len(ts) // 2], out
 
 
-def solve_case(p_t, n, T, nu, cycle="V", reps=5):
+def solve_case(p_t, n, T, nu, cycle="V", reps=5, coarsest=2, coarse="auto"):
     rhs = problems.seeded_rhs_batch_device(p_t, n, T, 42, (None,))[0]
-    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(p_t), T / n, n, coarsest=2)
-    cfg = tmg.CycleConfig(nu1=nu, nu2=nu, eps=1e-8, cycle=cycle)
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(p_t), T / n, n, coarsest=coarsest)
+    cfg = tmg.CycleConfig(nu1=nu, nu2=nu, eps=1e-8, cycle=cycle, coarse=coarse)
     u = torch.zeros_like(rhs)
     floor = 1e-12 * float(torch.linalg.norm(rhs))
 
@@ -70,7 +70,8 @@ def solve_case(p_t, n, T, nu, cycle="V", reps=5):
     run()
     best, med, st = timed(run, reps)
     dofs = n * (p_t + 1) * st.iterations
-    return {"p_t": p_t, "n": n, "T": T, "nu": nu, "cycle": cycle, "iterations": st.iterations,
+    return {"p_t": p_t, "n": n, "T": T, "nu": nu, "cycle": cycle, "coarsest": hier.levels[-1].n_steps,
+            "coarse_solver": coarse, "iterations": st.iterations,
             "best_s": best, "median_s": med, "time_dof_per_s": dofs / med,
             "final_norm": st.residual_norms[-1]}
 
@@ -137,9 +138,18 @@ def main():
     for r in out["config2"]:
         print("config2", r, flush=True)
     if not args.quick:
-        out["config4"] = [solve_case(2, 1 << 20, T, nu, cyc) for T in (1e-2, 1.0, 1e2)
-                          for nu in (1, 2) for cyc in ("V", "W")]
-        for r in out["config4"]:
+        # V down to 2 slabs (the reference setting); V and W over a 1024-slab
+        # coarsest level solved by the parallel scan (a deep W-cycle visits the
+        # 2-slab level 2^19 times per cycle -- inherently sequential, see DESIGN)
+        out["config4"] = []
+        for T in (1e-2, 1.0, 1e2):
+            for nu in (1, 2):
+                out["config4"].append(solve_case(2, 1 << 20, T, nu, "V"))
+                out["config4"].append(solve_case(2, 1 << 20, T, nu, "V", coarsest=1024, coarse="scan"))
+                out["config4"].append(solve_case(2, 1 << 20, T, nu, "W", coarsest=1024, coarse="scan",
+                                                 reps=3))
+        out["config4_deepW"] = [solve_case(2, 1 << 14, 1.0, 1, "W", reps=2)]
+        for r in out["config4"] + out["config4_deepW"]:
             print("config4", r, flush=True)
     out["config5"] = config5()
     for k, v in out["config5"].items():

@@ -73,7 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    objdir = os.path.join(CSRC, "obj")
+    # objects stay outside the tree (they need not travel with the snapshot)
+    objdir = os.environ.get("TMG_OBJDIR", "/tmp/tmg_b200_obj")
     os.makedirs(objdir, exist_ok=True)
 
     def compile_unit(unit):

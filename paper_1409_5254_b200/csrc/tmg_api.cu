@@ -64,6 +64,49 @@ bool sync_debug()
     return v == 1;
 }
 
+// TMG_EVENT_TRACE=1: direct launches with a CUDA event after each kernel;
+// solve() prints per-kernel device times (including launch gaps) to stderr
+bool event_trace()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TMG_EVENT_TRACE");
+        v = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+std::vector<std::pair<std::string, cudaEvent_t>> g_trace;
+void trace_mark(const char *what, cudaStream_t s)
+{
+    if (!event_trace()) return;
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    g_trace.emplace_back(what, e);
+}
+void trace_report()
+{
+    if (!event_trace() || g_trace.size() < 2) return;
+    cudaEventSynchronize(g_trace.back().second);
+    std::vector<std::pair<std::string, double>> agg;
+    double total = 0;
+    for (size_t i = 1; i < g_trace.size(); ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, g_trace[i - 1].second, g_trace[i].second);
+        total += ms;
+        bool found = false;
+        for (auto &a : agg)
+            if (a.first == g_trace[i].first) { a.second += ms; found = true; }
+        if (!found) agg.emplace_back(g_trace[i].first, ms);
+    }
+    fprintf(stderr, "event-trace total %.3f ms over %zu launches\n", total, g_trace.size() - 1);
+    for (auto &a : agg) fprintf(stderr, "event-trace %10.3f ms  %s\n", a.second, a.first.c_str());
+    for (auto &e : g_trace) cudaEventDestroy(e.second);
+    g_trace.clear();
+}
+
 #define CK_LAUNCH(what)                                                                  \
     do {                                                                                 \
         CK(cudaGetLastError());                                                          \
@@ -194,6 +237,7 @@ int launch_stream(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
     char what[96];
     snprintf(what, sizeof what, "stream_kernel<nt=%d,nu=%d,kind=%d> n=%lld flags=%d", NT, nu, kind, a.n, a.flags);
     CK_LAUNCH(what);
+    trace_mark(what, s);
     return 0;
 }
 
@@ -447,24 +491,34 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     }
 
     // one cycle's launches (multigrid.py:263-330 for gamma = 1)
-    int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s)
+    // down pass of level l (nu1 sweeps + residual + restriction); with_norm:
+    // also the numpy-order norm leaves of its INPUT (finest level, solve mode)
+    int enqueue_down(int l, const void *f0, void *u0, bool first_visit, bool with_norm, cudaStream_t s)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
-        // down
-        {
-            StreamArgs<T> a = stream_args<T>(n[l], B, 1);
-            a.f = fL;
-            const bool zero = (l > 0) && first_visit;
-            a.u_in = l == 0 ? (const T *)u0 : (zero ? nullptr : uA[l]);
-            a.u_out = uB[l];
-            a.fc = fl[l + 1];
-            a.active = d_active;
-            a.flags = SF_RESTRICT | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
-            if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-            CKR((launch_stream<T, NT>(L[l], a, o.nu1, K_DOWN, pk[l], SP, s)));
-            ++kernels_per_cycle;
+        StreamArgs<T> a = stream_args<T>(n[l], B, with_norm ? leaf_rows0 : 1);
+        a.f = fL;
+        const bool zero = (l > 0) && first_visit;
+        a.u_in = l == 0 ? (const T *)u0 : (zero ? nullptr : uA[l]);
+        a.u_out = uB[l];
+        a.fc = fl[l + 1];
+        a.active = d_active;
+        a.flags = SF_RESTRICT | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
+        if (with_norm) {
+            a.flags |= SF_NORM_LEAF;
+            a.leaf_out = leaves;
         }
-        // coarse-grid correction
+        if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+        CKR((launch_stream<T, NT>(L[l], a, o.nu1, with_norm ? K_DOWNNORM : K_DOWN, pk[l], SP, s)));
+        ++kernels_per_cycle;
+        return 0;
+    }
+
+    // coarse-grid correction of level l and its up pass (norm_up: the up pass
+    // also produces the norm of its output -- used when the down pass cannot)
+    int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s)
+    {
+        const T *fL = l == 0 ? (const T *)f0 : fl[l];
         if (l + 1 == tl) {
             TailArgs<T, NT> t = targ;
             t.f_in = fl[tl];
@@ -475,31 +529,39 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.active = d_active;
             CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");
+            trace_mark("tail_kernel", s);
             ++kernels_per_cycle;
         } else {
             for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s));
         }
-        // up
-        {
-            const bool leaf = norm && leaf_rows0 > 0;
-            StreamArgs<T> a = stream_args<T>(n[l], B, leaf ? leaf_rows0 : 1);
-            a.f = fL;
-            a.u_in = uB[l];
-            a.uc = uA[l + 1];
-            a.u_out = l == 0 ? (T *)u0 : uA[l];
-            a.active = d_active;
-            a.flags = SF_PROLONG | SF_WRITE_U;
-            if (norm) {
-                if (leaf) { a.flags |= SF_NORM_LEAF; a.leaf_out = leaves; }
-                else { a.flags |= SF_NORM_SQ; a.sq_out = sqbuf; }
-            }
-            if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
-            const int kind = norm ? (leaf ? K_UPNORM : K_GENERIC) : K_UP;
-            CKR((launch_stream<T, NT>(L[l], a, o.nu2, kind, pk[l], SP, s)));
-            ++kernels_per_cycle;
+        const bool leaf = norm_up && leaf_rows0 > 0;
+        StreamArgs<T> a = stream_args<T>(n[l], B, leaf ? leaf_rows0 : 1);
+        a.f = fL;
+        a.u_in = uB[l];
+        a.uc = uA[l + 1];
+        a.u_out = l == 0 ? (T *)u0 : uA[l];
+        a.active = d_active;
+        a.flags = SF_PROLONG | SF_WRITE_U;
+        if (norm_up) {
+            if (leaf) { a.flags |= SF_NORM_LEAF; a.leaf_out = leaves; }
+            else { a.flags |= SF_NORM_SQ; a.sq_out = sqbuf; }
         }
+        if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
+        const int kind = norm_up ? (leaf ? K_UPNORM : K_GENERIC) : K_UP;
+        CKR((launch_stream<T, NT>(L[l], a, o.nu2, kind, pk[l], SP, s)));
+        ++kernels_per_cycle;
         return 0;
     }
+
+    int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s)
+    {
+        CKR(enqueue_down(l, f0, u0, first_visit, false, s));
+        return enqueue_rest(l, f0, u0, norm, s);
+    }
+
+    // the finest down pass computes the stopping norm of its input (the
+    // previous cycle's result) when the norm has numpy's leaf structure
+    bool norm_in() const { return leaf_rows0 > 0 && SP; }
 
     int enqueue_finalize(int mode, double eps, cudaStream_t s, cudaGraphConditionalHandle h = 0,
                          bool use_h = false)
@@ -511,8 +573,10 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             finalize_sq_kernel<<<(unsigned)B, 1024, 0, s>>>(sqbuf, n[0], d_st, d_hist, hist_stride, d_floor,
                                                            eps, mode, nullptr);
         CK_LAUNCH("finalize");
+        trace_mark("finalize", s);
         set_active_kernel<<<1, 256, 0, s>>>(d_st, d_active, d_any, (int)B, h, use_h ? 1 : 0);
         CK_LAUNCH("set_active");
+        trace_mark("set_active", s);
         kernels_per_cycle += 2;
         return 0;
     }
@@ -521,7 +585,14 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                       cudaGraphConditionalHandle h = 0, bool use_h = false)
     {
         kernels_per_cycle = 0;
-        CKR(enqueue_level(0, f, u, true, norm, s));
+        if (norm && norm_in()) {
+            // rest of this cycle, then the NEXT cycle's finest down pass, whose
+            // first sweep yields ||f - L u|| of this cycle's result
+            CKR(enqueue_rest(0, f, u, false, s));
+            CKR(enqueue_down(0, f, u, true, true, s));
+        } else {
+            CKR(enqueue_level(0, f, u, true, norm, s));
+        }
         if (norm) CKR(enqueue_finalize(1, eps, s, h, use_h));
         return 0;
     }
@@ -531,15 +602,19 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                        bool use_h = false)
     {
         CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));
-        const bool leaf = leaf_rows0 > 0;
-        StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
-        a.f = (const T *)f;
-        a.u_in = (const T *)u;
-        a.flags = leaf ? SF_NORM_LEAF : SF_NORM_SQ;
-        a.leaf_out = leaves;
-        a.sq_out = sqbuf;
-        if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-        CKR((launch_stream<T, NT>(L[0], a, 0, K_GENERIC, P_GEN, SP, s)));
+        if (norm_in()) {
+            CKR(enqueue_down(0, f, u, true, true, s));  // the first cycle's down pass
+        } else {
+            const bool leaf = leaf_rows0 > 0;
+            StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
+            a.f = (const T *)f;
+            a.u_in = (const T *)u;
+            a.flags = leaf ? SF_NORM_LEAF : SF_NORM_SQ;
+            a.leaf_out = leaves;
+            a.sq_out = sqbuf;
+            if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+            CKR((launch_stream<T, NT>(L[0], a, 0, K_GENERIC, P_GEN, SP, s)));
+        }
         return enqueue_finalize(0, eps, s, h, use_h);
     }
 
@@ -593,7 +668,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     int run_cycle(const void *f, void *u, bool norm, double eps, cudaStream_t s)
     {
-        if (!o.use_graph || sync_debug()) return enqueue_cycle(f, u, norm, eps, s);
+        if (!o.use_graph || sync_debug() || event_trace()) return enqueue_cycle(f, u, norm, eps, s);
         if (!gexec || g_f != f || g_u != u || g_norm != norm || g_eps != eps) {
             if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
             cudaGraph_t g;
@@ -774,11 +849,12 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.active = nullptr;
             CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");
-        } else if (o.use_graph && !sync_debug() && !getenv("TMG_NO_SOLVE_GRAPH")) {
+        } else if (o.use_graph && !sync_debug() && !event_trace() && !getenv("TMG_NO_SOLVE_GRAPH")) {
             if (!sexec || s_f != f || s_u != u || s_eps != eps || s_hist != hist_stride)
                 CKR(build_solve_graph(f, u, eps));
             CK(cudaGraphLaunch(sexec, s));
         } else {
+            trace_mark("start", s);
             CKR(enqueue_prefix(f, u, eps, s));
             CK(cudaMemcpyAsync(h_any, d_any, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -799,6 +875,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     int collect()
     {
         CK(cudaEventSynchronize(ev_done));
+        trace_report();
         h_hist.assign(hp_hist, hp_hist + (size_t)hist_stride * B);
         h_it.resize(B);
         h_conv.resize(B);

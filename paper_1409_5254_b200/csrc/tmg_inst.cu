@@ -73,6 +73,7 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
     case K_DOWN: return by_perm<T, NT, K_DOWN>(L, a, nu, perm, s);
     case K_UP: return by_perm<T, NT, K_UP>(L, a, nu, perm, s);
     case K_UPNORM: return by_perm<T, NT, K_UPNORM>(L, a, nu, perm, s);
+    case K_DOWNNORM: return by_perm<T, NT, K_DOWNNORM>(L, a, nu, perm, s);
     }
     return -1;
 }

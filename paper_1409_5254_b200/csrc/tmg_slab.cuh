@@ -495,20 +495,16 @@ template <typename T, int NT> __device__ __forceinline__ void lu_apply_ieee(cons
     }
 }
 
-// J independent slabs (one per row of a stage) swept together: two dependency
-// chains per lane hide the fp64 latency of the strictly ordered arithmetic
-template <typename T, int NT, bool SPARSE, int PERM, int J>
-__device__ __forceinline__ void sweep_j(const LevelC<T, NT> &L, T (&u)[J][NT], const T (&f)[J][NT],
-                                        const Cpl<T, NT, SPARSE> (&p)[J], const bool (&hp)[J])
+// LU solve + damped update for J slabs whose permuted residuals y are given
+template <typename T, int NT, int J>
+__device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], T (&y)[J][NT])
 {
-    T y[J][NT], ys[J][NT];
+    T ys[J][NT];
     unsigned bad = 0;
 #pragma unroll
-    for (int q = 0; q < J; ++q) {
-        residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], p[q], hp[q], y[q]);
+    for (int q = 0; q < J; ++q)
 #pragma unroll
         for (int i = 0; i < NT; ++i) ys[q][i] = y[q][i];
-    }
 #pragma unroll
     for (int q = 0; q < J; ++q) lu_apply_nb<T, NT>(L, y[q], bad);
     if (__any_sync(0xffffffffu, bad)) {
@@ -523,6 +519,39 @@ __device__ __forceinline__ void sweep_j(const LevelC<T, NT> &L, T (&u)[J][NT], c
     for (int q = 0; q < J; ++q)
 #pragma unroll
         for (int i = 0; i < NT; ++i) u[q][i] = FP<T>::add(FP<T>::mul(y[q][i], L.omega), u[q][i]);
+}
+
+// J independent slabs (one per row of a stage) swept together: two dependency
+// chains per lane hide the fp64 latency of the strictly ordered arithmetic
+template <typename T, int NT, bool SPARSE, int PERM, int J>
+__device__ __forceinline__ void sweep_j(const LevelC<T, NT> &L, T (&u)[J][NT], const T (&f)[J][NT],
+                                        const Cpl<T, NT, SPARSE> (&p)[J], const bool (&hp)[J])
+{
+    T y[J][NT];
+#pragma unroll
+    for (int q = 0; q < J; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], p[q], hp[q], y[q]);
+    finish_j<T, NT, J>(L, u, y);
+}
+
+// undo the row permutation of residual_perm: r[perm[i]] = y[i]
+template <typename T, int NT, int PERM>
+__device__ __forceinline__ void unpermute(const LevelC<T, NT> &L, const T (&y)[NT], T (&r)[NT])
+{
+    if constexpr (PERM == P_ROT) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) r[j] = y[(j + NT - 1) % NT];
+    } else if constexpr (PERM == P_ID) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) r[j] = y[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            T v = y[0];
+#pragma unroll
+            for (int i = 1; i < NT; ++i) v = (L.perm[i] == j) ? y[i] : v;
+            r[j] = v;
+        }
+    }
 }
 
 template <typename T, int NT, bool SPARSE, int PERM>

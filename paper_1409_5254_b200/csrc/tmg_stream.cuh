@@ -28,7 +28,7 @@
 namespace tmg {
 
 constexpr int SW_WARPS = 8;   // warps per CTA
-constexpr int SW_STAGES = 3;  // ring stages per warp
+constexpr int SW_STAGES = 4;  // ring stages per warp (3 for the up passes: larger stages)
 constexpr int SW_GROUP = 2;   // rows per stage
 
 enum StreamFlags : int {
@@ -43,7 +43,10 @@ enum StreamFlags : int {
 };
 
 // kernel specialisations: the plan's hot passes get their flags at compile time
-enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3 };
+// K_DOWNNORM: a down pass that also returns the residual norm of its INPUT
+// (taken from the first sweep's residual -- the stopping test of the previous
+// cycle comes for free with the next cycle's first pass)
+enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM = 4 };
 
 template <typename T> struct StreamArgs {
     const T *f;
@@ -121,25 +124,35 @@ template <typename T, int NT, bool WITH_C> struct RowLayout {
     static constexpr int OFF_F = SW_GROUP * ROW;
     static constexpr int OFF_C = 2 * SW_GROUP * ROW;
     static constexpr int STAGE = SW_GROUP * (2 * ROW + (WITH_C ? HALF : 0));
+    // ring depth from a per-CTA budget that keeps the register-limited
+    // occupancy (3 CTAs/SM for n_t <= 2, 2 CTAs/SM above): 2..4 stages
+    static constexpr size_t BUDGET = NT <= 2 ? 72 * 1024 : 100 * 1024;
+    static constexpr int ST_RAW = (int)(BUDGET / (SW_WARPS * sizeof(T) * STAGE));
+    static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > SW_STAGES ? SW_STAGES : ST_RAW);
     // per-warp copy of (R1, R2) for n_t >= 3 (R2 padded by 2 elements so the
     // even and odd half-warps read different banks)
     static constexpr int RELEMS = NT >= 3 ? 2 * NT * NT + 2 : 0;
     static constexpr int RSTRIDE = NT * NT + 2;
     static constexpr size_t RBYTES = ((sizeof(T) * RELEMS + 15) / 16) * 16;
-    static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * SW_STAGES + RBYTES;
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * ST + RBYTES;
     // mbarrier block (one 8-byte barrier per warp and stage), padded to 128 B
-    static constexpr size_t BAR_BYTES = ((SW_WARPS * SW_STAGES * 8 + 127) / 128) * 128;
+    static constexpr size_t BAR_BYTES = ((SW_WARPS * ST * 8 + 127) / 128) * 128;
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * SW_WARPS;
 };
 
-template <int KIND> struct KindProlongs { static constexpr bool value = KIND != K_DOWN; };
+template <int KIND> struct KindProlongs {
+    static constexpr bool value = KIND != K_DOWN && KIND != K_DOWNNORM;
+};
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct Streamer {
     using C = Cpl<T, NT, SPARSE>;
     static constexpr int CF = KIND == K_DOWN ? (SF_RESTRICT | SF_WRITE_U)
                               : KIND == K_UP ? (SF_PROLONG | SF_WRITE_U)
                               : KIND == K_UPNORM ? (SF_PROLONG | SF_WRITE_U | SF_NORM_LEAF)
-                                                 : 0;
+                              : KIND == K_DOWNNORM ? (SF_RESTRICT | SF_WRITE_U | SF_NORM_LEAF)
+                                                   : 0;
+    // norm of the pass's input (K_DOWNNORM) rather than of its output
+    static constexpr bool NORM_IN = KIND == K_DOWNNORM && NU > 0;
     // rows swept jointly per lane (two dependency chains hide fp64 latency);
     // larger blocks have enough independent work per row already
     static constexpr int J = NT <= 2 ? 2 : 1;
@@ -149,7 +162,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     int flags;
     // this lane's transfer block (odd lanes R2, even lanes R1): registers for
     // n_t <= 2, a per-warp shared-memory copy for larger blocks
-    static constexpr bool RREG = NT <= 2;
+    static constexpr bool RREG = NT * NT * sizeof(T) <= 64;
     T Rm[RREG ? NT * NT : 1];
     const T *Rs;
     C carry[NU + 1];    // lane 0: predecessor data of the next row, per sweep
@@ -164,6 +177,31 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     __device__ __forceinline__ bool need_r() const
     {
         return has(SF_RESTRICT) || has(SF_NORM_LEAF) || has(SF_NORM_SQ) || has(SF_WRITE_R);
+    }
+
+    // numpy pairwise leaf (np.sum, multigrid.py:459): accumulator j sums leaf
+    // elements j, j+8, j+16, ... in order; 8 accumulators combined as
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) at the leaf's last row
+    __device__ __forceinline__ void leaf_add(const T (&r)[NT], long long row, int b)
+    {
+        T sq = sqnorm<T, NT>(r);
+        T v1 = __shfl_down_sync(0xffffffffu, sq, 8);
+        T v2 = __shfl_down_sync(0xffffffffu, sq, 16);
+        T v3 = __shfl_down_sync(0xffffffffu, sq, 24);
+        leaf_acc = (leaf_q == 0) ? sq : FP<T>::add(leaf_acc, sq);
+        leaf_acc = FP<T>::add(leaf_acc, v1);
+        leaf_acc = FP<T>::add(leaf_acc, v2);
+        leaf_acc = FP<T>::add(leaf_acc, v3);
+        if (leaf_q == a.leaf_rows - 1) {
+            T t1 = FP<T>::add(leaf_acc, __shfl_down_sync(0xffffffffu, leaf_acc, 1));
+            T t2 = FP<T>::add(t1, __shfl_down_sync(0xffffffffu, t1, 2));
+            T t3 = FP<T>::add(t2, __shfl_down_sync(0xffffffffu, t2, 4));
+            const long long nleaves = a.n / (32LL * a.leaf_rows);
+            if (lane == 0) a.leaf_out[(size_t)b * nleaves + row / a.leaf_rows] = (double)t3;
+            leaf_q = 0;
+        } else {
+            leaf_q += 1;
+        }
     }
 
     // predecessor data for JJ consecutive rows at sweep k (rotate-shuffle + carry)
@@ -210,7 +248,25 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         for (int k = 0; k < NU; ++k) {
             C prev[JJ];
             exchange<JJ>(u, k, prev);
-            sweep_j<T, NT, SPARSE, PERM, JJ>(L, u, f, prev, hp);
+            if (NORM_IN && k == 0) {
+                // the first sweep's residual IS the input's residual: take its norm
+                T y[JJ][NT];
+#pragma unroll
+                for (int q = 0; q < JJ; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], prev[q], hp[q], y[q]);
+                if (!warm) {
+#pragma unroll
+                    for (int q = 0; q < JJ; ++q) {
+                        if (INTERIOR || q < nrow) {
+                            T r[NT];
+                            unpermute<T, NT, PERM>(L, y[q], r);
+                            leaf_add(r, row_idx0 + q, b);
+                        }
+                    }
+                }
+                finish_j<T, NT, JJ>(L, u, y);
+            } else {
+                sweep_j<T, NT, SPARSE, PERM, JJ>(L, u, f, prev, hp);
+            }
         }
         if (need_r()) {
             C prev[JJ];
@@ -237,29 +293,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                     if (has(SF_NORM_SQ)) {
                         if (valid[q]) a.sq_out[(size_t)b * a.n + sl] = (double)sqnorm<T, NT>(r);
                     }
-                    if (has(SF_NORM_LEAF) && (INTERIOR || q < nrow)) {
-                        // numpy pairwise leaf (np.sum, multigrid.py:459): accumulator
-                        // j sums leaf elements j, j+8, j+16, ... in order
-                        T sq = sqnorm<T, NT>(r);
-                        T v1 = __shfl_down_sync(0xffffffffu, sq, 8);
-                        T v2 = __shfl_down_sync(0xffffffffu, sq, 16);
-                        T v3 = __shfl_down_sync(0xffffffffu, sq, 24);
-                        leaf_acc = (leaf_q == 0) ? sq : FP<T>::add(leaf_acc, sq);
-                        leaf_acc = FP<T>::add(leaf_acc, v1);
-                        leaf_acc = FP<T>::add(leaf_acc, v2);
-                        leaf_acc = FP<T>::add(leaf_acc, v3);
-                        if (leaf_q == a.leaf_rows - 1) {
-                            T t1 = FP<T>::add(leaf_acc, __shfl_down_sync(0xffffffffu, leaf_acc, 1));
-                            T t2 = FP<T>::add(t1, __shfl_down_sync(0xffffffffu, t1, 2));
-                            T t3 = FP<T>::add(t2, __shfl_down_sync(0xffffffffu, t2, 4));
-                            const long long nleaves = a.n / (32LL * a.leaf_rows);
-                            if (lane == 0)
-                                a.leaf_out[(size_t)b * nleaves + (row_idx0 + q) / a.leaf_rows] = (double)t3;
-                            leaf_q = 0;
-                        } else {
-                            leaf_q += 1;
-                        }
-                    }
+                    if (!NORM_IN && has(SF_NORM_LEAF) && (INTERIOR || q < nrow)) leaf_add(r, row_idx0 + q, b);
                 }
             }
         }
@@ -311,7 +345,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
     const T *ub = zero_guess ? nullptr : a.u_in + (size_t)b * n * NT;
     const T *ucb = prolong ? a.uc + (size_t)b * st.nc * NT : nullptr;
 
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * SW_STAGES;
+    constexpr int ST = Lay::ST;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * ST;
     unsigned char *wbase = smem + Lay::BAR_BYTES + (size_t)warp * Lay::BYTES_PER_WARP;
     T *ring = reinterpret_cast<T *>(wbase + Lay::RBYTES);
     if (st.has(SF_RESTRICT) || prolong) {
@@ -341,15 +376,15 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
     uint64_t pol = 0;
     if (lane == 0 && tma) {
 #pragma unroll
-        for (int s = 0; s < SW_STAGES; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         pol = policy_evict_first();
     }
     __syncwarp();
     auto issue = [&](int g) {  // lane 0 only
         if (!group_tma(g)) return;
-        T *stg = ring + (size_t)(g % SW_STAGES) * Lay::STAGE;
-        uint64_t *bar = &bars[g % SW_STAGES];
+        T *stg = ring + (size_t)(g % ST) * Lay::STAGE;
+        uint64_t *bar = &bars[g % ST];
         const long long s0 = (row0 + (long long)g * G) * 32;
         const uint32_t bytes = (uint32_t)(G * Lay::ROW * sizeof(T));
         const uint32_t cbytes = prolong ? (uint32_t)(G * Lay::HALF * sizeof(T)) : 0u;
@@ -359,7 +394,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
         if (cbytes) bulk_g2s(stg + Lay::OFF_C, ucb + (s0 >> 1) * NT, cbytes, bar, pol);
     };
     if (lane == 0 && tma)
-        for (int g = 0; g < ngroups && g < SW_STAGES; ++g) issue(g);
+        for (int g = 0; g < ngroups && g < ST; ++g) issue(g);
 
     // warm-up: the J rows before the chunk, for the carries only
     if (row0 > 0) {
@@ -380,11 +415,11 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
 
     for (int g = 0; g < ngroups; ++g) {
         const bool gt = group_tma(g);
-        const T *stg = ring + (size_t)(g % SW_STAGES) * Lay::STAGE;
+        const T *stg = ring + (size_t)(g % ST) * Lay::STAGE;
         const long long r0g = row0 + (long long)g * G;
         const int nrow = min(G, rows - g * G);
         const bool interior = r0g > 0 && (r0g + G) * 32 <= n && nrow == G;
-        if (gt) mbar_wait(&bars[g % SW_STAGES], (uint32_t)((g / SW_STAGES) & 1));
+        if (gt) mbar_wait(&bars[g % ST], (uint32_t)((g / ST) & 1));
 #pragma unroll
         for (int q0 = 0; q0 < G; q0 += J) {
             T u[J][NT], f[J][NT], uc[J][NT];
@@ -412,7 +447,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
             if (q0 + J >= G) {
                 // the stage is fully read: hand it back to the copy engine
                 __syncwarp();
-                if (gt && lane == 0 && g + SW_STAGES < ngroups) issue(g + SW_STAGES);
+                if (gt && lane == 0 && g + ST < ngroups) issue(g + ST);
             }
             if (q0 < nrow) {
                 if (interior)

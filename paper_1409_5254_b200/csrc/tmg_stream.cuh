@@ -30,6 +30,9 @@ namespace tmg {
 constexpr int SW_WARPS = 8;   // warps per CTA
 constexpr int SW_STAGES = 4;  // ring stages per warp (3 for the up passes: larger stages)
 constexpr int SW_GROUP = 2;   // rows per stage
+#ifndef TMG_MINB
+#define TMG_MINB(NT) 2
+#endif
 
 enum StreamFlags : int {
     SF_ZERO_GUESS = 1,   // u_in is the zero vector: not read
@@ -313,7 +316,7 @@ __device__ __forceinline__ void load_row(const T *src, T (&x)[NT], bool vec)
 }
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM>
-__global__ void __launch_bounds__(SW_WARPS * 32, NT <= 2 ? 3 : 2)
+__global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     stream_kernel(const __grid_constant__ LevelC<T, NT> L, const __grid_constant__ StreamArgs<T> a)
 {
     constexpr bool WITH_C = KindProlongs<KIND>::value;

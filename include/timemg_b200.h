@@ -128,6 +128,14 @@ typedef struct tmg_plan_opts {
 /* levels: n_levels descriptors (the cycle depth), finest first. */
 int tmg_plan_create(tmg_plan **plan, const tmg_level_desc *levels, int n_levels, int64_t batch,
                     const tmg_plan_opts *opts);
+/* A batch of problems with DIFFERENT operators of the same shape (levels:
+ * batch x n_levels descriptors, problem-major), e.g. a sweep of the two-grid
+ * convergence factor over (p_t-fixed) step sizes and damping values
+ * (measure_convergence_factor, multigrid.py:534-544; the paper's Fourier-vs-
+ * measured experiment).  Supported when a whole problem fits one CTA
+ * (TMG_E_UNSUPPORTED otherwise); solve/stats as for tmg_plan_create. */
+int tmg_plan_create_multi(tmg_plan **plan, const tmg_level_desc *levels, int n_levels, int64_t batch,
+                          const tmg_plan_opts *opts);
 int tmg_plan_destroy(tmg_plan *plan);
 
 /* One or more cycles without norms (v_cycle / two_grid_cycle,

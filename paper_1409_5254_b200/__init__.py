@@ -10,6 +10,7 @@ from .assembly import (ALPHA_MIN, BasisSpec, BlockLU, GlobalSystem, LocalOperato
                        stability_function)
 from .hierarchy import CycleConfig, Level, SolveStats, TimeHierarchy
 from .solver import (DevicePlan, block_jacobi_sweep, forward_solve, measure_convergence_factor,
+                     measure_convergence_factors, rhs_moments_device,
                      random_initial_guess, solve, solve_batched, two_grid_cycle, v_cycle)
 
 __version__ = "0.1.0"

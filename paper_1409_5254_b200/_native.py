@@ -103,6 +103,7 @@ _lib = None
 
 EXPORTS = ("tmg_last_error", "tmg_version", "tmg_device_check", "tmg_sweep", "tmg_residual",
            "tmg_down", "tmg_up", "tmg_coarse_solve", "tmg_resid_norm", "tmg_plan_create",
+           "tmg_plan_create_multi",
            "tmg_plan_destroy", "tmg_plan_cycles", "tmg_plan_solve", "tmg_plan_solve_host",
            "tmg_plan_stats", "tmg_plan_info")
 
@@ -129,6 +130,7 @@ def load():
     L.tmg_coarse_solve.argtypes = [ci, lp, vp, vp, i64, ci, ci, vp]
     L.tmg_resid_norm.argtypes = [ci, lp, vp, vp, vp, i64, vp]
     L.tmg_plan_create.argtypes = [ctypes.POINTER(vp), lp, ci, i64, ctypes.POINTER(PlanOpts)]
+    L.tmg_plan_create_multi.argtypes = [ctypes.POINTER(vp), lp, ci, i64, ctypes.POINTER(PlanOpts)]
     L.tmg_plan_destroy.argtypes = [vp]
     L.tmg_plan_cycles.argtypes = [vp, vp, vp, ci, vp]
     L.tmg_plan_solve.argtypes = [vp, vp, vp, dp, ctypes.c_double, ci, vp]

@@ -392,7 +392,9 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     size_t fixed_smem() const { return tail_fixed_smem<T, NT>(depth - tl); }
 
-    int init(const tmg_level_desc *lv, int nl, long long batch, const tmg_plan_opts &opts)
+    // multi: lv holds batch x nl descriptors -- a different operator per
+    // problem (same level sizes); only whole-problem-in-one-CTA plans
+    int init(const tmg_level_desc *lv, int nl, long long batch, const tmg_plan_opts &opts, bool multi = false)
     {
         depth = nl;
         B = batch;
@@ -409,8 +411,20 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         CK(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-        CK(cudaMalloc(&d_levels, sizeof(LevelC<T, NT>) * nl));
-        CK(cudaMemcpy(d_levels, L.data(), sizeof(LevelC<T, NT>) * nl, cudaMemcpyHostToDevice));
+        if (multi) {
+            std::vector<LevelC<T, NT>> all;
+            for (long long b = 0; b < batch; ++b)
+                for (int l = 0; l < nl; ++l) {
+                    if (lv[b * nl + l].n_slabs != n[l] || lv[b * nl + l].n_t != NT)
+                        return fail(TMG_E_ARG, "problem %lld level %d: sizes differ from problem 0", b, l);
+                    all.push_back(make_level<T, NT>(lv[b * nl + l]));
+                }
+            CK(cudaMalloc(&d_levels, sizeof(LevelC<T, NT>) * all.size()));
+            CK(cudaMemcpy(d_levels, all.data(), sizeof(LevelC<T, NT>) * all.size(), cudaMemcpyHostToDevice));
+        } else {
+            CK(cudaMalloc(&d_levels, sizeof(LevelC<T, NT>) * nl));
+            CK(cudaMemcpy(d_levels, L.data(), sizeof(LevelC<T, NT>) * nl, cudaMemcpyHostToDevice));
+        }
 
         // choose the tail: the longest suffix of small levels that fits in smem
         const size_t smem_cap = 200 * 1024;
@@ -478,6 +492,10 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         targ.nu2 = o.nu2;
         targ.gamma = o.gamma;
         targ.dot_variant = o.dot_variant;
+        targ.levels_stride = multi ? nl : 0;
+        if (multi && tl != 0)
+            return fail(TMG_E_UNSUPPORTED, "per-problem operators need the whole problem in one CTA "
+                                           "(at most %lld slabs here)", tail_max);
         targ.trace = nullptr;
         if (getenv("TMG_TAIL_TRACE")) {
             CK(cudaMalloc(&d_trace, sizeof(unsigned long long) * 6 * MAXLEV));
@@ -916,15 +934,18 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
 template <typename T, int NT>
 int make_plan_sp(std::unique_ptr<PlanBase> &out, const tmg_level_desc *lv, int nl, long long B,
-                 const tmg_plan_opts &o)
+                 const tmg_plan_opts &o, bool multi)
 {
-    if (coupling_is_sparse(lv[0])) {
+    bool sparse = true;
+    for (long long b = 0; b < (multi ? B : 1); ++b)
+        for (int l = 0; l < nl; ++l) sparse &= coupling_is_sparse(lv[b * nl + l]);
+    if (sparse) {
         auto p = std::make_unique<Plan<T, NT, true>>();
-        CKR(p->init(lv, nl, B, o));
+        CKR(p->init(lv, nl, B, o, multi));
         out = std::move(p);
     } else {
         auto p = std::make_unique<Plan<T, NT, false>>();
-        CKR(p->init(lv, nl, B, o));
+        CKR(p->init(lv, nl, B, o, multi));
         out = std::move(p);
     }
     return 0;
@@ -932,13 +953,13 @@ int make_plan_sp(std::unique_ptr<PlanBase> &out, const tmg_level_desc *lv, int n
 
 template <typename T>
 int make_plan_t(std::unique_ptr<PlanBase> &out, const tmg_level_desc *lv, int nl, long long B,
-                const tmg_plan_opts &o)
+                const tmg_plan_opts &o, bool multi = false)
 {
     switch (lv[0].n_t) {
-    case 1: return make_plan_sp<T, 1>(out, lv, nl, B, o);
-    case 2: return make_plan_sp<T, 2>(out, lv, nl, B, o);
-    case 3: return make_plan_sp<T, 3>(out, lv, nl, B, o);
-    case 4: return make_plan_sp<T, 4>(out, lv, nl, B, o);
+    case 1: return make_plan_sp<T, 1>(out, lv, nl, B, o, multi);
+    case 2: return make_plan_sp<T, 2>(out, lv, nl, B, o, multi);
+    case 3: return make_plan_sp<T, 3>(out, lv, nl, B, o, multi);
+    case 4: return make_plan_sp<T, 4>(out, lv, nl, B, o, multi);
     }
     return fail(TMG_E_UNSUPPORTED, "n_t=%d", lv[0].n_t);
 }
@@ -1175,6 +1196,29 @@ int tmg_plan_create(tmg_plan **plan, const tmg_level_desc *levels, int n_levels,
     int rc;
     if (opts->dtype == TMG_F64) rc = make_plan_t<double>(p->impl, levels, n_levels, batch, *opts);
     else if (opts->dtype == TMG_F32) rc = make_plan_t<float>(p->impl, levels, n_levels, batch, *opts);
+    else return fail(TMG_E_ARG, "unknown dtype");
+    if (rc) return rc;
+    *plan = p.release();
+    return 0;
+}
+
+int tmg_plan_create_multi(tmg_plan **plan, const tmg_level_desc *levels, int n_levels, int64_t batch,
+                          const tmg_plan_opts *opts)
+{
+    if (!plan || !levels || !opts) return fail(TMG_E_ARG, "NULL argument");
+    *plan = nullptr;
+    if (n_levels < 2 || n_levels > MAXLEV) return fail(TMG_E_ARG, "need 2..%d levels, got %d", MAXLEV, n_levels);
+    if (batch < 1) return fail(TMG_E_ARG, "batch must be >= 1");
+    for (long long i = 0; i < batch * n_levels; ++i) {
+        CKR(check_desc(&levels[i]));
+        if (levels[i].n_t != levels[0].n_t) return fail(TMG_E_ARG, "problems disagree on n_t");
+    }
+    if (opts->nu1 < 0 || opts->nu2 < 0 || opts->nu1 + opts->nu2 < 1)
+        return fail(TMG_E_ARG, "need nu1, nu2 >= 0 with nu1 + nu2 >= 1");
+    auto p = std::make_unique<tmg_plan>();
+    int rc;
+    if (opts->dtype == TMG_F64) rc = make_plan_t<double>(p->impl, levels, n_levels, batch, *opts, true);
+    else if (opts->dtype == TMG_F32) rc = make_plan_t<float>(p->impl, levels, n_levels, batch, *opts, true);
     else return fail(TMG_E_ARG, "unknown dtype");
     if (rc) return rc;
     *plan = p.release();

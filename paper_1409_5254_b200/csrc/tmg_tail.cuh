@@ -467,7 +467,7 @@ __device__ void tail_body(const TailArgs<T, NT> &a)
     const int nlev = a.depth - a.l0;
     // constants and level metadata into shared memory
     for (int i = threadIdx.x; i < (int)(sizeof(LevelC<T, NT>) * nlev / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tmg_tail_smem)[i] = reinterpret_cast<const uint32_t *>(a.levels + a.l0)[i];
+        reinterpret_cast<uint32_t *>(tmg_tail_smem)[i] = reinterpret_cast<const uint32_t *>(a.levels + (size_t)b * a.levels_stride + a.l0)[i];
     Engine<T, NT, SPARSE, SMEM> E;
     E.l0 = a.l0;
     E.nthr = blockDim.x;

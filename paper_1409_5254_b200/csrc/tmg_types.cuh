@@ -29,6 +29,7 @@ template <typename T, int NT> struct TailArgs {
     int in_smem;
     int nu1, nu2, gamma, dot_variant;
     int coarse_scan;              // coarsest solve by the CTA scan (not bitwise)
+    int levels_stride;            // 0: one operator for the batch; else problem b's levels at b*stride
     unsigned long long *trace;    // optional: per-phase SM-cycle totals of problem 0 (diagnostics)
     int full;                     // 1: _iterate with norms; 0: n_cycles cycles
     int n_cycles;

@@ -56,30 +56,24 @@ def kernel_inputs(n_steps: int, n_t: int, seed: int = 0):
 
 def seeded_rhs_batch_device(p_t: int, n_steps: int, T: float = 1.0, seed=42, batch_indices=(0,),
                             device="cuda"):
-    """The seeded problems of ``seeded_rhs`` assembled on the GPU in float64
-    (same quadrature formula as rhs_moments, dg.py:265-287, evaluated with
-    torch ops).  Used to build large benchmark batches quickly; values agree
-    with the host assembly to a few ulp (the parity tests use host inputs).
-    Returns a (B, n_steps, p_t + 1) float64 CUDA tensor."""
+    """The seeded problems of ``seeded_rhs`` assembled on the GPU
+    (solver.rhs_moments_device).  Used to build large benchmark batches
+    quickly; values agree with the host assembly to a few ulp (the parity
+    tests use host inputs).  Returns a (B, n_steps, p_t + 1) float64 tensor."""
     import torch
 
-    from .assembly import basis_values, radau_rule
+    from .solver import rhs_moments_device
 
     basis = BasisSpec(p_t)
-    rule = radau_rule(basis.n_t)
-    tau = T / n_steps
-    weights = torch.from_numpy(tau * basis_values(basis, rule.c) * rule.b).to(device)  # (n_t, s)
-    c = torch.from_numpy(rule.c).to(device)
-    start = torch.from_numpy(basis_values(basis, np.array([0.0]))[:, 0]).to(device)
-    times = (torch.arange(n_steps, device=device, dtype=torch.float64)[:, None] + c[None, :]) * tau
     out = torch.empty((len(batch_indices), n_steps, basis.n_t), dtype=torch.float64, device=device)
     for i, b in enumerate(batch_indices):
         a, phi, u0 = forcing_params(seed, b)
-        fv = torch.zeros_like(times)
-        for k in range(8):
-            fv += a[k] * torch.sin(2.0 * np.pi * (k + 1) * times / T + phi[k])
-        rhs = fv @ weights.T
-        if u0 != 0.0:
-            rhs[0] += u0 * start
-        out[i] = rhs
+
+        def f(t, a=a, phi=phi):
+            v = torch.zeros_like(t)
+            for k in range(8):
+                v += a[k] * torch.sin(2.0 * np.pi * (k + 1) * t / T + phi[k])
+            return v
+
+        out[i] = rhs_moments_device(f, basis, T / n_steps, n_steps, u0=u0, device=device)
     return out

@@ -98,28 +98,39 @@ def _out(t, was_torch):
     return t.cpu().numpy()
 
 
+def _level_descs(hier, level0, depth, omegas):
+    levels = hier.levels[level0:level0 + depth]
+    out = []
+    for i, lev in enumerate(levels):
+        last = i + 1 == depth
+        out.append(nat.level_desc(lev.ops, lev.n_steps, omegas[i],
+                                  None if last else lev.r1, None if last else lev.r2))
+    return out
+
+
 class DevicePlan:
-    """A tmg_plan: level constants, per-level device buffers, launch schedule."""
+    """A tmg_plan: level constants, per-level device buffers, launch schedule.
+    ``multi`` (a list of (hier, omegas) pairs): one operator per problem."""
 
     def __init__(self, hier, level0: int, depth: int, omegas, config: CycleConfig, batch: int,
-                 dtype: int = nat.F64, use_graph: bool = True):
+                 dtype: int = nat.F64, use_graph: bool = True, multi=None):
         lib = nat.load()
-        levels = hier.levels[level0:level0 + depth]
-        descs = (nat.LevelDesc * depth)()
-        for i, lev in enumerate(levels):
-            last = i + 1 == depth
-            descs[i] = nat.level_desc(lev.ops, lev.n_steps, omegas[i],
-                                      None if last else lev.r1, None if last else lev.r2)
+        if multi is None:
+            flat = _level_descs(hier, level0, depth, omegas)
+        else:
+            flat = [d for h, om in multi for d in _level_descs(h, level0, depth, om)]
+        descs = (nat.LevelDesc * len(flat))(*flat)
         self.depth = depth
         self.batch = batch
-        self.n0 = levels[0].n_steps
-        self.n_t = levels[0].ops.n_t
+        self.n0 = flat[0].n_slabs
+        self.n_t = flat[0].n_t
         self.dtype = dtype
         opts = nat.PlanOpts(dtype, config.nu1, config.nu2, 2 if config.cycle == "W" else 1,
                             _COARSE[config.coarse], int(config.dot_variant), int(use_graph),
                             int(TAIL_MAX))
         self._h = ctypes.c_void_p()
-        nat.check(lib.tmg_plan_create(ctypes.byref(self._h), descs, depth, batch, ctypes.byref(opts)),
+        create = lib.tmg_plan_create if multi is None else lib.tmg_plan_create_multi
+        nat.check(create(ctypes.byref(self._h), descs, depth, batch, ctypes.byref(opts)),
                   "tmg_plan_create")
 
     def __del__(self):
@@ -417,3 +428,47 @@ def measure_convergence_factor(hier, config: CycleConfig = None) -> float:
     it, norms, conv = plan.solve(fd, ud, [0.0], config.eps, min(config.max_iters, 250))
     k = int(it[0])
     return max_ratio([float(v) for v in norms[0, :k + 1]])
+
+
+def measure_convergence_factors(basis, taus, nu=1, n_steps: int = 1024, damping="optimal",
+                                seed: int = 42, eps: float = 1e-100, max_iters: int = 250):
+    """Two-grid convergence factors for many step sizes in ONE launch:
+    factor[i] == measure_convergence_factor(TimeHierarchy.build(basis, taus[i],
+    n_steps, n_levels=2), CycleConfig(nu1=nu, nu2=nu, damping=damping,
+    eps=eps, seed=seed, max_iters=max_iters)) bit for bit (multigrid.py:534-544;
+    the paper's measured-vs-predicted experiment, tests/test_acceptance.py:45-59).
+    Each problem carries its own operator; one CTA per problem."""
+    from .hierarchy import TimeHierarchy
+    taus = list(taus)
+    cfg = CycleConfig(nu1=nu, nu2=nu, damping=damping, eps=eps, seed=seed, max_iters=max_iters)
+    hiers = [TimeHierarchy.build(basis, float(t), n_steps, n_levels=2) for t in taus]
+    multi = [(h, omegas_for(h, cfg, 2)) for h in hiers]
+    plan = DevicePlan(hiers[0], 0, 2, multi[0][1], cfg, len(hiers), multi=multi)
+    u0 = random_initial_guess(hiers[0], seed)
+    U = np.ascontiguousarray(np.broadcast_to(u0, (len(hiers),) + u0.shape))
+    F = np.zeros_like(U)
+    _check_device()
+    it, norms, conv = plan.solve_host(F, U, U, np.zeros(len(hiers)), eps, min(max_iters, 250))
+    return [max_ratio([float(v) for v in norms[b, :int(it[b]) + 1]]) for b in range(len(hiers))]
+
+
+def rhs_moments_device(f, basis, tau: float, n_steps: int, u0: float = 0.0, t0: float = 0.0,
+                       device: str = "cuda"):
+    """rhs_moments (dg.py:265-287) evaluated on the GPU: ``f`` takes a float64
+    CUDA tensor of times and returns values of the same shape (torch ops).
+    Left Radau quadrature of order 2 p_t + 1, u0 folded into slab 0.  Agrees
+    with the host assembly to a few ulp (transcendentals differ between numpy
+    and CUDA); returns a (n_steps, n_t) float64 CUDA tensor."""
+    torch = _torch()
+    from .assembly import basis_values, radau_rule
+    rule = radau_rule(basis.n_t)
+    weights = torch.from_numpy(tau * basis_values(basis, rule.c) * rule.b).to(device)
+    c = torch.from_numpy(rule.c).to(device)
+    times = t0 + (torch.arange(n_steps, device=device, dtype=torch.float64)[:, None] + c[None, :]) * tau
+    fv = f(times)
+    if not torch.is_tensor(fv) or fv.shape != times.shape:
+        raise TypeError("f must map a (n_steps, s) float64 tensor to values of the same shape")
+    rhs = fv.to(torch.float64) @ weights.T
+    if u0 != 0.0:
+        rhs[0] += u0 * torch.from_numpy(basis_values(basis, np.array([0.0]))[:, 0]).to(device)
+    return rhs

@@ -403,3 +403,37 @@ def test_w_cycle_large_coarsest_scan(oracle_mod):
     assert st.iterations == iters
     assert np.linalg.norm(u - ur) <= 1e-12 * np.linalg.norm(ur)
     assert np.allclose(st.residual_norms, norms, rtol=1e-9, atol=0)
+
+
+def test_measure_convergence_factors_batched(golden):
+    """many step sizes in one launch (one operator per problem) == one
+    measure_convergence_factor call per step size, bit for bit"""
+    man, _ = golden
+    for c in man["factors"]:
+        basis = tmg.BasisSpec(c["p_t"])
+        taus = [c["tau"], 1e-3, 1.0, 1e3]
+        got = tmg.measure_convergence_factors(basis, taus, nu=c["nu"], max_iters=150)
+        assert got[0] == c["factor"], c
+        for t, g in zip(taus[1:], got[1:]):
+            hier = tmg.TimeHierarchy.build(basis, t, 1024, n_levels=2)
+            one = tmg.measure_convergence_factor(
+                hier, tmg.CycleConfig(nu1=c["nu"], nu2=c["nu"], eps=1e-100, seed=42, max_iters=150))
+            assert g == one, (c, t)
+
+
+def test_rhs_moments_device_close_to_host():
+    import torch
+    a, phi, u0 = problems.forcing_params(42)
+    for p_t in range(4):
+        basis = tmg.BasisSpec(p_t)
+        n, T = 4096, 1.0
+        host = tmg.rhs_moments(problems.make_forcing(a, phi, T), basis, T / n, n, u0=u0)
+
+        def f(t):
+            v = torch.zeros_like(t)
+            for k in range(8):
+                v += a[k] * torch.sin(2.0 * np.pi * (k + 1) * t / T + phi[k])
+            return v
+
+        dev = tmg.rhs_moments_device(f, basis, T / n, n, u0=u0).cpu().numpy()
+        assert np.max(np.abs(dev - host)) <= 1e-14 * np.max(np.abs(host))

@@ -248,7 +248,7 @@ int chunk_rows(long long n, long long batch, int leaf_rows)
     const long long rows = (n + 31) / 32;
     const long long target_warps = (long long)sm_count() * 16 * 4;
     long long r = (rows * batch) / std::max(1LL, target_warps);
-    r = std::max(4LL, std::min(64LL, r));
+    r = std::max(4LL, std::min(128LL, r));
     // multiple of the ring group (2 rows) and of the norm leaf
     const int q = leaf_rows == 3 ? 6 : (leaf_rows == 1 || leaf_rows == 2 || leaf_rows == 4 ? 4 : 2 * std::max(1, leaf_rows));
     r = ((r + q - 1) / q) * q;

@@ -230,9 +230,12 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     // JJ rows starting at slab0 (this lane's slab in the first row);
     // INTERIOR: every slab exists and none is slab 0 of the problem.
     // Rows q >= nrow are beyond the chunk: computed but never stored.
+    // uo/fco: this lane's u_out / f_coarse element for the first row (row
+    // stride 32*NT / 16*NT elements), advanced by the caller
     template <bool INTERIOR, int JJ>
     __device__ __forceinline__ void rows(T (&u)[JJ][NT], const T (&f)[JJ][NT], const T (&uc)[JJ][NT],
-                                         long long slab0, long long row_idx0, int nrow, bool warm, int b)
+                                         long long slab0, long long row_idx0, int nrow, bool warm, int b,
+                                         T *uo, T *fco)
     {
         bool valid[JJ], hp[JJ];
 #pragma unroll
@@ -291,7 +294,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                         for (int i = 0; i < NT; ++i) p[i] = FP<T>::add(p[i], qq[i]);
                         const long long cidx = sl >> 1;
                         if (!(lane & 1) && (INTERIOR || (valid[q] && cidx < nc)))
-                            store_slab<T, NT>(a.fc + ((size_t)b * nc + cidx) * NT, p);
+                            store_slab<T, NT>(fco + q * 16 * NT, p);
                     }
                     if (has(SF_NORM_SQ)) {
                         if (valid[q]) a.sq_out[(size_t)b * a.n + sl] = (double)sqnorm<T, NT>(r);
@@ -303,7 +306,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         if (has(SF_WRITE_U) && !warm) {
 #pragma unroll
             for (int q = 0; q < JJ; ++q)
-                if (valid[q]) store_slab<T, NT>(a.u_out + ((size_t)b * a.n + slab0 + 32 * q) * NT, u[q]);
+                if (valid[q]) store_slab<T, NT>(uo + q * 32 * NT, u[q]);
         }
     }
 };
@@ -372,10 +375,14 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     st.leaf_acc = T(0);
     st.leaf_q = 0;
 
-    // a group goes through the ring iff it consists of G whole rows
-    auto group_tma = [&](int g) -> bool {
-        return tma && (g + 1) * G <= rows && (row0 + (long long)(g + 1) * G) * 32 <= n;
-    };
+    // groups [0, g_full) consist of G whole rows (and go through the ring when
+    // TMA is on); groups [g_int0, g_full) are interior (no slab 0, all valid)
+    const int g_full = (int)max(0LL, min((long long)(rows / G), (n / 32 - row0) / G));
+    const int g_int0 = row0 == 0 ? 1 : 0;
+    auto group_tma = [&](int g) -> bool { return tma && g < g_full; };
+    // per-lane output cursors (advanced by G rows per group)
+    T *uo = st.has(SF_WRITE_U) ? a.u_out + ((size_t)b * n + (size_t)row0 * 32 + lane) * NT : nullptr;
+    T *fco = st.has(SF_RESTRICT) ? a.fc + ((size_t)b * st.nc + (size_t)row0 * 16 + (lane >> 1)) * NT : nullptr;
     uint64_t pol = 0;
     if (lane == 0 && tma) {
 #pragma unroll
@@ -412,8 +419,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
             if (!zero_guess) load_row<T, NT>(ub + sl * NT, u[q], tma);
             if (prolong) load_row<T, NT>(ucb + (sl >> 1) * NT, uc[q], tma);
         }
-        if (wr0 > 0) st.template rows<true, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b);
-        else st.template rows<false, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b);
+        if (wr0 > 0) st.template rows<true, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr);
+        else st.template rows<false, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr);
     }
 
     for (int g = 0; g < ngroups; ++g) {
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
         const T *stg = ring + (size_t)(g % ST) * Lay::STAGE;
         const long long r0g = row0 + (long long)g * G;
         const int nrow = min(G, rows - g * G);
-        const bool interior = r0g > 0 && (r0g + G) * 32 <= n && nrow == G;
+        const bool interior = g >= g_int0 && g < g_full;
         if (gt) mbar_wait(&bars[g % ST], (uint32_t)((g / ST) & 1));
 #pragma unroll
         for (int q0 = 0; q0 < G; q0 += J) {
@@ -454,10 +461,13 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
             }
             if (q0 < nrow) {
                 if (interior)
-                    st.template rows<true, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, J, false, b);
+                    st.template rows<true, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, J, false, b, uo, fco);
                 else
-                    st.template rows<false, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, nrow - q0, false, b);
+                    st.template rows<false, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, nrow - q0, false, b,
+                                               uo, fco);
             }
+            uo += J * 32 * NT;
+            fco += J * 16 * NT;
         }
     }
 }

@@ -248,9 +248,9 @@ int chunk_rows(long long n, long long batch, int leaf_rows)
     const long long rows = (n + 31) / 32;
     const long long target_warps = (long long)sm_count() * 16 * 4;
     long long r = (rows * batch) / std::max(1LL, target_warps);
-    r = std::max(4LL, std::min(128LL, r));
+    r = std::max(2LL, std::min(128LL, r));
     // multiple of the ring group (2 rows) and of the norm leaf
-    const int q = leaf_rows == 3 ? 6 : (leaf_rows == 1 || leaf_rows == 2 || leaf_rows == 4 ? 4 : 2 * std::max(1, leaf_rows));
+    const int q = leaf_rows == 3 ? 6 : (leaf_rows == 4 ? 4 : 2);
     r = ((r + q - 1) / q) * q;
     return (int)std::max<long long>(r, 1);
 }
@@ -323,7 +323,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     std::vector<LevelC<T, NT>> L;
     std::vector<int> pk;  // LU permutation pattern per level
     LevelC<T, NT> *d_levels = nullptr;
-    std::vector<T *> uA, uB, fl;
+    std::vector<T *> uA, uB, fl, halo;
+    bool up2 = false;  // up passes recompute the pre-sweeps (nu1 == nu2): no stored pre-smoothed u
     int tl = 0;                 // first tail level
     bool tail_smem = true;
     size_t tail_smem_bytes = 0;
@@ -362,6 +363,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         for (auto p : uA) cudaFree(p);
         for (auto p : uB) cudaFree(p);
         for (auto p : fl) cudaFree(p);
+        for (auto p : halo) cudaFree(p);
         cudaFree(d_levels);
         if (d_trace) {
             std::vector<unsigned long long> tr(6 * MAXLEV);
@@ -464,6 +466,15 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         }
         // norm machinery (finest level)
         leaf_rows0 = leaf_rows_for(n[0]);
+        up2 = SP && o.nu1 == o.nu2 && o.nu1 >= 1 && o.nu1 <= 4 && !getenv("TMG_NO_UP2");
+        halo.assign(nl, nullptr);
+        if (up2) {
+            const int J = stream_joint_rows<T, NT>();
+            for (int l = 0; l < tl; ++l) {
+                StreamArgs<T> a = level_args(l);
+                CK(cudaMalloc(&halo[l], sizeof(T) * (size_t)B * a.chunks * J * 32 * NT + 16));
+            }
+        }
         if (leaf_rows0) {
             nleaves = n[0] / (32LL * leaf_rows0);
             CK(cudaMalloc(&leaves, sizeof(double) * nleaves * B));
@@ -509,16 +520,24 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     }
 
     // one cycle's launches (multigrid.py:263-330 for gamma = 1)
+    // chunking of level l, identical for its down and up passes (the halo
+    // and the warm-up rows must line up); the finest level follows the norm leaves
+    StreamArgs<T> level_args(int l) const
+    {
+        return stream_args<T>(n[l], B, l == 0 && leaf_rows0 > 0 ? leaf_rows0 : 1);
+    }
+
     // down pass of level l (nu1 sweeps + residual + restriction); with_norm:
     // also the numpy-order norm leaves of its INPUT (finest level, solve mode)
     int enqueue_down(int l, const void *f0, void *u0, bool first_visit, bool with_norm, cudaStream_t s)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
-        StreamArgs<T> a = stream_args<T>(n[l], B, with_norm ? leaf_rows0 : 1);
+        StreamArgs<T> a = up2 ? level_args(l) : stream_args<T>(n[l], B, with_norm ? leaf_rows0 : 1);
         a.f = fL;
         const bool zero = (l > 0) && first_visit;
         a.u_in = l == 0 ? (const T *)u0 : (zero ? nullptr : uA[l]);
-        a.u_out = uB[l];
+        a.u_out = up2 ? nullptr : uB[l];
+        a.halo = up2 ? halo[l] : nullptr;
         a.fc = fl[l + 1];
         a.active = d_active;
         a.flags = SF_RESTRICT | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
@@ -534,7 +553,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     // coarse-grid correction of level l and its up pass (norm_up: the up pass
     // also produces the norm of its output -- used when the down pass cannot)
-    int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s)
+    int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s, bool first_visit = true)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
         if (l + 1 == tl) {
@@ -551,6 +570,23 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             ++kernels_per_cycle;
         } else {
             for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s));
+        }
+        if (up2 && !norm_up) {
+            // prolong-add + post-sweeps, the pre-sweeps recomputed from the
+            // level's original iterate (read in place; warm-ups from the halo)
+            StreamArgs<T> a = level_args(l);
+            const bool zero = (l > 0) && first_visit;
+            a.f = fL;
+            a.u_in = l == 0 ? (const T *)u0 : (zero ? nullptr : uA[l]);
+            a.uc = uA[l + 1];
+            a.u_out = l == 0 ? (T *)u0 : uA[l];
+            a.halo = halo[l];
+            a.active = d_active;
+            a.flags = SF_PROLONG | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
+            if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
+            CKR((launch_stream<T, NT>(L[l], a, o.nu2, K_UP2, pk[l], SP, s)));
+            ++kernels_per_cycle;
+            return 0;
         }
         const bool leaf = norm_up && leaf_rows0 > 0;
         StreamArgs<T> a = stream_args<T>(n[l], B, leaf ? leaf_rows0 : 1);
@@ -573,8 +609,31 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s)
     {
+        if (up2 && norm) {
+            // the up pass cannot produce the norm: take it in a separate pass
+            CKR(enqueue_down(l, f0, u0, first_visit, false, s));
+            CKR(enqueue_rest(l, f0, u0, false, s, first_visit));
+            return enqueue_norm_pass(f0, u0, s);
+        }
         CKR(enqueue_down(l, f0, u0, first_visit, false, s));
-        return enqueue_rest(l, f0, u0, norm, s);
+        return enqueue_rest(l, f0, u0, norm, s, first_visit);
+    }
+
+    // standalone ||f - L u|| pass at the finest level (r0 / generic sizes)
+    int enqueue_norm_pass(const void *f, void *u, cudaStream_t s)
+    {
+        const bool leaf = leaf_rows0 > 0;
+        StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
+        a.f = (const T *)f;
+        a.u_in = (const T *)u;
+        a.active = d_active;
+        a.flags = leaf ? SF_NORM_LEAF : SF_NORM_SQ;
+        a.leaf_out = leaves;
+        a.sq_out = sqbuf;
+        if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
+        CKR((launch_stream<T, NT>(L[0], a, 0, K_GENERIC, P_GEN, SP, s)));
+        ++kernels_per_cycle;
+        return 0;
     }
 
     // the finest down pass computes the stopping norm of its input (the
@@ -620,19 +679,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                        bool use_h = false)
     {
         CK(cudaMemsetAsync(d_active, 0xff, sizeof(int) * B, s));
-        if (norm_in()) {
-            CKR(enqueue_down(0, f, u, true, true, s));  // the first cycle's down pass
-        } else {
-            const bool leaf = leaf_rows0 > 0;
-            StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
-            a.f = (const T *)f;
-            a.u_in = (const T *)u;
-            a.flags = leaf ? SF_NORM_LEAF : SF_NORM_SQ;
-            a.leaf_out = leaves;
-            a.sq_out = sqbuf;
-            if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
-            CKR((launch_stream<T, NT>(L[0], a, 0, K_GENERIC, P_GEN, SP, s)));
-        }
+        if (norm_in()) CKR(enqueue_down(0, f, u, true, true, s));  // the first cycle's down pass
+        else CKR(enqueue_norm_pass(f, u, s));
         return enqueue_finalize(0, eps, s, h, use_h);
     }
 

@@ -74,11 +74,14 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
     case K_UP: return by_perm<T, NT, K_UP>(L, a, nu, perm, s);
     case K_UPNORM: return by_perm<T, NT, K_UPNORM>(L, a, nu, perm, s);
     case K_DOWNNORM: return by_perm<T, NT, K_DOWNNORM>(L, a, nu, perm, s);
+    case K_UP2: return by_perm<T, NT, K_UP2>(L, a, nu, perm, s);
     }
     return -1;
 }
 
 template <typename T, int NT> size_t stream_smem_bytes() { return RowLayout<T, NT, true>::SMEM_BYTES; }
+template <typename T, int NT> int stream_joint_rows() { return JointRows<T, NT>::value; }
+template int stream_joint_rows<TMG_T, TMG_NT>();
 
 template <typename T, int NT> int tail_prepare(bool sparse, size_t smem)
 {

@@ -49,7 +49,10 @@ enum StreamFlags : int {
 // K_DOWNNORM: a down pass that also returns the residual norm of its INPUT
 // (taken from the first sweep's residual -- the stopping test of the previous
 // cycle comes for free with the next cycle's first pass)
-enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM = 4 };
+// K_UP2: an up pass that RECOMPUTES the nu pre-sweeps from the level's
+// original iterate (bitwise the same values the down pass had) instead of
+// reading a stored pre-smoothed iterate -- the down pass then writes no u.
+enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM = 4, K_UP2 = 5 };
 
 template <typename T> struct StreamArgs {
     const T *f;
@@ -58,6 +61,8 @@ template <typename T> struct StreamArgs {
     const T *uc;
     T *fc;
     T *r_out;
+    T *halo;               // [batch][chunks][J rows][32][NT]: each chunk's last J rows of the
+                           // ORIGINAL iterate (written by down passes, read by K_UP2 warm-ups)
     double *sq_out;
     double *leaf_out;
     const int *active;
@@ -146,6 +151,11 @@ template <typename T, int NT, bool WITH_C> struct RowLayout {
 template <int KIND> struct KindProlongs {
     static constexpr bool value = KIND != K_DOWN && KIND != K_DOWNNORM;
 };
+// rows processed jointly (must agree between a level's down and up passes:
+// the halo holds J rows)
+template <typename T, int NT> struct JointRows {
+    static constexpr int value = (NT <= 2 || sizeof(T) == 4) ? 2 : 1;
+};
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct Streamer {
     using C = Cpl<T, NT, SPARSE>;
@@ -153,12 +163,15 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                               : KIND == K_UP ? (SF_PROLONG | SF_WRITE_U)
                               : KIND == K_UPNORM ? (SF_PROLONG | SF_WRITE_U | SF_NORM_LEAF)
                               : KIND == K_DOWNNORM ? (SF_RESTRICT | SF_WRITE_U | SF_NORM_LEAF)
-                                                   : 0;
+                              : KIND == K_UP2 ? (SF_PROLONG | SF_WRITE_U)
+                                              : 0;
+    // pre-sweeps recomputed before the prolongation (K_UP2)
+    static constexpr int NPRE = KIND == K_UP2 ? NU : 0;
     // norm of the pass's input (K_DOWNNORM) rather than of its output
     static constexpr bool NORM_IN = KIND == K_DOWNNORM && NU > 0;
     // rows swept jointly per lane (two dependency chains hide fp64 latency);
     // larger blocks have enough independent work per row already
-    static constexpr int J = NT <= 2 ? 2 : 1;
+    static constexpr int J = JointRows<T, NT>::value;
     const LevelC<T, NT> &L;
     const StreamArgs<T> &a;
     int lane;
@@ -168,10 +181,11 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     static constexpr bool RREG = NT * NT * sizeof(T) <= 64;
     T Rm[RREG ? NT * NT : 1];
     const T *Rs;
-    C carry[NU + 1];    // lane 0: predecessor data of the next row, per sweep
+    C carry[NPRE + NU + 1];  // lane 0: predecessor data of the next row, per sweep
     T leaf_acc;
     int leaf_q;         // row position inside the current numpy leaf
     long long nc;
+    bool write_u;       // the pass stores u (u_out given)
 
     __device__ __forceinline__ bool has(int f) const
     {
@@ -243,6 +257,17 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
             const long long sl = slab0 + 32 * q;
             valid[q] = INTERIOR || (q < nrow && sl < a.n);
             hp[q] = INTERIOR || sl > 0;
+        }
+        // K_UP2: the down pass's pre-sweeps, recomputed (same bits)
+#pragma unroll
+        for (int k = 0; k < NPRE; ++k) {
+            C prev[JJ];
+            exchange<JJ>(u, k, prev);
+            sweep_j<T, NT, SPARSE, PERM, JJ>(L, u, f, prev, hp);
+        }
+#pragma unroll
+        for (int q = 0; q < JJ; ++q) {
+            const long long sl = slab0 + 32 * q;
             if (has(SF_PROLONG)) {
                 if (INTERIOR || sl < 2 * nc) {
                     if constexpr (RREG) prolong_reg<T, NT>(Rm, uc[q], u[q]);
@@ -253,7 +278,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
 #pragma unroll
         for (int k = 0; k < NU; ++k) {
             C prev[JJ];
-            exchange<JJ>(u, k, prev);
+            exchange<JJ>(u, NPRE + k, prev);
             if (NORM_IN && k == 0) {
                 // the first sweep's residual IS the input's residual: take its norm
                 T y[JJ][NT];
@@ -276,7 +301,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         }
         if (need_r()) {
             C prev[JJ];
-            exchange<JJ>(u, NU, prev);
+            exchange<JJ>(u, NPRE + NU, prev);
             if (!warm) {
 #pragma unroll
                 for (int q = 0; q < JJ; ++q) {
@@ -303,7 +328,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                 }
             }
         }
-        if (has(SF_WRITE_U) && !warm) {
+        if (has(SF_WRITE_U) && !warm && write_u) {
 #pragma unroll
             for (int q = 0; q < JJ; ++q)
                 if (valid[q]) store_slab<T, NT>(uo + q * 32 * NT, u[q]);
@@ -371,7 +396,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
         }
     }
 #pragma unroll
-    for (int k = 0; k <= NU; ++k) cpl_zero(st.carry[k]);
+    for (int k = 0; k <= S::NPRE + NU; ++k) cpl_zero(st.carry[k]);
     st.leaf_acc = T(0);
     st.leaf_q = 0;
 
@@ -381,7 +406,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     const int g_int0 = row0 == 0 ? 1 : 0;
     auto group_tma = [&](int g) -> bool { return tma && g < g_full; };
     // per-lane output cursors (advanced by G rows per group)
-    T *uo = st.has(SF_WRITE_U) ? a.u_out + ((size_t)b * n + (size_t)row0 * 32 + lane) * NT : nullptr;
+    st.write_u = st.has(SF_WRITE_U) && a.u_out != nullptr;
+    T *uo = st.write_u ? a.u_out + ((size_t)b * n + (size_t)row0 * 32 + lane) * NT : nullptr;
     T *fco = st.has(SF_RESTRICT) ? a.fc + ((size_t)b * st.nc + (size_t)row0 * 16 + (lane >> 1)) * NT : nullptr;
     uint64_t pol = 0;
     if (lane == 0 && tma) {
@@ -416,7 +442,13 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
             zero_slab<T, NT>(u[q]);
             zero_slab<T, NT>(uc[q]);
             load_row<T, NT>(fb + sl * NT, f[q], tma);
-            if (!zero_guess) load_row<T, NT>(ub + sl * NT, u[q], tma);
+            if (!zero_guess) {
+                if (S::NPRE > 0)  // the neighbour chunk may already have overwritten these rows
+                    load_row<T, NT>(a.halo + (((size_t)b * a.chunks + chunk - 1) * J + q) * 32 * NT + lane * NT,
+                                    u[q], tma);
+                else
+                    load_row<T, NT>(ub + sl * NT, u[q], tma);
+            }
             if (prolong) load_row<T, NT>(ucb + (sl >> 1) * NT, uc[q], tma);
         }
         if (wr0 > 0) st.template rows<true, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr);
@@ -454,6 +486,16 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
                     }
                 }
             }
+            if (a.halo && !zero_guess && chunk + 1 < a.chunks && !S::NPRE) {
+                // last J rows of the chunk: the next chunk's up-pass warm-up input
+#pragma unroll
+                for (int q = 0; q < J; ++q) {
+                    const int rr = g * G + q0 + q;
+                    if (rr >= rows - J && rr < rows)
+                        store_slab<T, NT>(a.halo + (((size_t)b * a.chunks + chunk) * J + (rr - (rows - J))) * 32 * NT +
+                                              lane * NT, u[q]);
+                }
+            }
             if (q0 + J >= G) {
                 // the stage is fully read: hand it back to the copy engine
                 __syncwarp();
@@ -466,8 +508,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
                     st.template rows<false, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, nrow - q0, false, b,
                                                uo, fco);
             }
-            uo += J * 32 * NT;
-            fco += J * 16 * NT;
+            if (st.write_u) uo += J * 32 * NT;
+            if (fco) fco += J * 16 * NT;
         }
     }
 }

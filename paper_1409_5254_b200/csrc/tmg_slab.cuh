@@ -533,6 +533,35 @@ __device__ __forceinline__ void sweep_j(const LevelC<T, NT> &L, T (&u)[J][NT], c
     finish_j<T, NT, J>(L, u, y);
 }
 
+// the first sweep from the zero initial guess: with u = +0 the residual equals
+// f up to the signs of zero entries, which cannot change any nonzero value of
+// the LU solve, and the update (c omega) + (+0) maps every zero to +0 -- so
+// u = (omega LU^-1 f) + 0 is bitwise the full sweep, without the matrix
+// products and without the predecessor exchange
+template <typename T, int NT, int PERM, int J>
+__device__ __forceinline__ void sweep_zero_j(const LevelC<T, NT> &L, T (&u)[J][NT], const T (&f)[J][NT])
+{
+    T y[J][NT];
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        if constexpr (PERM == P_GEN) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                T v = f[q][0];
+#pragma unroll
+                for (int c = 1; c < NT; ++c) v = (L.perm[i] == c) ? f[q][c] : v;
+                y[q][i] = v;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) y[q][i] = f[q][(PERM == P_ROT) ? (i + 1) % NT : i];
+        }
+#pragma unroll
+        for (int i = 0; i < NT; ++i) u[q][i] = T(0);
+    }
+    finish_j<T, NT, J>(L, u, y);
+}
+
 // undo the row permutation of residual_perm: r[perm[i]] = y[i]
 template <typename T, int NT, int PERM>
 __device__ __forceinline__ void unpermute(const LevelC<T, NT> &L, const T (&y)[NT], T (&r)[NT])

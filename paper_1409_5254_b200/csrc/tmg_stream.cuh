@@ -249,7 +249,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     template <bool INTERIOR, int JJ>
     __device__ __forceinline__ void rows(T (&u)[JJ][NT], const T (&f)[JJ][NT], const T (&uc)[JJ][NT],
                                          long long slab0, long long row_idx0, int nrow, bool warm, int b,
-                                         T *uo, T *fco)
+                                         T *uo, T *fco, bool zg)
     {
         bool valid[JJ], hp[JJ];
 #pragma unroll
@@ -261,6 +261,10 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         // K_UP2: the down pass's pre-sweeps, recomputed (same bits)
 #pragma unroll
         for (int k = 0; k < NPRE; ++k) {
+            if (k == 0 && zg) {
+                sweep_zero_j<T, NT, PERM, JJ>(L, u, f);
+                continue;
+            }
             C prev[JJ];
             exchange<JJ>(u, k, prev);
             sweep_j<T, NT, SPARSE, PERM, JJ>(L, u, f, prev, hp);
@@ -277,6 +281,10 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         }
 #pragma unroll
         for (int k = 0; k < NU; ++k) {
+            if (!NORM_IN && NPRE == 0 && k == 0 && zg) {
+                sweep_zero_j<T, NT, PERM, JJ>(L, u, f);
+                continue;
+            }
             C prev[JJ];
             exchange<JJ>(u, NPRE + k, prev);
             if (NORM_IN && k == 0) {
@@ -451,8 +459,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
             }
             if (prolong) load_row<T, NT>(ucb + (sl >> 1) * NT, uc[q], tma);
         }
-        if (wr0 > 0) st.template rows<true, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr);
-        else st.template rows<false, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr);
+        if (wr0 > 0) st.template rows<true, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr, zero_guess);
+        else st.template rows<false, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr, zero_guess);
     }
 
     for (int g = 0; g < ngroups; ++g) {
@@ -503,10 +511,11 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
             }
             if (q0 < nrow) {
                 if (interior)
-                    st.template rows<true, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, J, false, b, uo, fco);
+                    st.template rows<true, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, J, false, b, uo, fco,
+                                              zero_guess);
                 else
                     st.template rows<false, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, nrow - q0, false, b,
-                                               uo, fco);
+                                               uo, fco, zero_guess);
             }
             if (st.write_u) uo += J * 32 * NT;
             if (fco) fco += J * 16 * NT;

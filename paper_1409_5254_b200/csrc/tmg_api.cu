@@ -22,6 +22,7 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <numeric>
 
 #include "timemg_b200.h"
 #include "tmg_launch.cuh"
@@ -241,28 +242,31 @@ int launch_stream(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
     return 0;
 }
 
-// rows per warp chunk: enough warps to fill the GPU several times over, a
-// multiple of the norm leaf, and long enough to amortise the warm-up row
-int chunk_rows(long long n, long long batch, int leaf_rows)
+// rows (of w slabs) per warp chunk: enough warps to fill the GPU several
+// times over, a multiple of the norm leaf, and long enough to amortise the
+// warm-up row
+int chunk_rows(long long n, long long batch, int leaf_rows, int w)
 {
-    const long long rows = (n + 31) / 32;
+    const long long rows = (n + w - 1) / w;
     const long long target_warps = (long long)sm_count() * 16 * 4;
     long long r = (rows * batch) / std::max(1LL, target_warps);
     r = std::max(2LL, std::min(128LL, r));
-    // multiple of the ring group (2 rows) and of the norm leaf
-    const int q = leaf_rows == 3 ? 6 : (leaf_rows == 4 ? 4 : 2);
+    // a multiple of the ring stage (64 slabs) and of the norm leaf
+    const int g = 64 / w;
+    const int q = std::lcm(g, std::max(leaf_rows, 1));
     r = ((r + q - 1) / q) * q;
     return (int)std::max<long long>(r, 1);
 }
 
-template <typename T> StreamArgs<T> stream_args(long long n, long long batch, int leaf_rows)
+template <typename T, int NT> StreamArgs<T> stream_args(long long n, long long batch, int leaf_rows)
 {
+    constexpr int w = 32 * slabs_per_lane<T, NT>();
     StreamArgs<T> a;
     memset(&a, 0, sizeof a);
     a.n = n;
     a.batch = (int)batch;
-    a.rows_per_chunk = chunk_rows(n, batch, leaf_rows);
-    a.chunks = ((n + 31) / 32 + a.rows_per_chunk - 1) / a.rows_per_chunk;
+    a.rows_per_chunk = chunk_rows(n, batch, leaf_rows, w);
+    a.chunks = ((n + w - 1) / w + a.rows_per_chunk - 1) / a.rows_per_chunk;
     a.leaf_rows = leaf_rows > 0 ? leaf_rows : 1;
     return a;
 }
@@ -281,16 +285,17 @@ template <typename T, int NT> bool tma_ok(const StreamArgs<T> &a, bool prolong)
 }
 
 // numpy pairwise leaf structure of an n-vector: n = m * 2^k with the recursion
-// splitting exactly in halves down to leaves of m <= 128 values
-int leaf_rows_for(long long n)
+// splitting exactly in halves down to leaves of m <= 128 values; the leaf path
+// of the streaming kernels needs whole rows of w slabs per leaf
+int leaf_rows_for(long long n, int w)
 {
     long long m = n;
     while (m > 128) {
         if (m % 2 || (m / 2) % 8) return 0;
         m /= 2;
     }
-    if (m % 32) return 0;
-    return (int)(m / 32);
+    if (m % w) return 0;
+    return (int)(m / w);
 }
 
 // ---------------------------------------------------------------------------
@@ -316,6 +321,7 @@ struct tmg_plan {
 namespace {
 
 template <typename T, int NT, bool SP> struct Plan : PlanBase {
+    static constexpr int ROWW = 32 * slabs_per_lane<T, NT>();  // slabs per streaming row
     int depth = 0;
     long long B = 0;
     tmg_plan_opts o{};
@@ -465,18 +471,17 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             if (l < tl) CK(cudaMalloc(&uB[l], bytes));
         }
         // norm machinery (finest level)
-        leaf_rows0 = leaf_rows_for(n[0]);
+        leaf_rows0 = leaf_rows_for(n[0], ROWW);
         up2 = SP && o.nu1 == o.nu2 && o.nu1 >= 1 && o.nu1 <= 4 && !getenv("TMG_NO_UP2");
         halo.assign(nl, nullptr);
         if (up2) {
-            const int J = stream_joint_rows<T, NT>();
             for (int l = 0; l < tl; ++l) {
                 StreamArgs<T> a = level_args(l);
-                CK(cudaMalloc(&halo[l], sizeof(T) * (size_t)B * a.chunks * J * 32 * NT + 16));
+                CK(cudaMalloc(&halo[l], sizeof(T) * (size_t)B * a.chunks * ROWW * NT + 16));
             }
         }
         if (leaf_rows0) {
-            nleaves = n[0] / (32LL * leaf_rows0);
+            nleaves = n[0] / ((long long)ROWW * leaf_rows0);
             CK(cudaMalloc(&leaves, sizeof(double) * nleaves * B));
         }
         CK(cudaMalloc(&sqbuf, sizeof(double) * n[0] * B));
@@ -524,7 +529,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     // and the warm-up rows must line up); the finest level follows the norm leaves
     StreamArgs<T> level_args(int l) const
     {
-        return stream_args<T>(n[l], B, l == 0 && leaf_rows0 > 0 ? leaf_rows0 : 1);
+        return stream_args<T, NT>(n[l], B, l == 0 && leaf_rows0 > 0 ? leaf_rows0 : 1);
     }
 
     // down pass of level l (nu1 sweeps + residual + restriction); with_norm:
@@ -532,7 +537,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     int enqueue_down(int l, const void *f0, void *u0, bool first_visit, bool with_norm, cudaStream_t s)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
-        StreamArgs<T> a = up2 ? level_args(l) : stream_args<T>(n[l], B, with_norm ? leaf_rows0 : 1);
+        StreamArgs<T> a = up2 ? level_args(l) : stream_args<T, NT>(n[l], B, with_norm ? leaf_rows0 : 1);
         a.f = fL;
         const bool zero = (l > 0) && first_visit;
         a.u_in = l == 0 ? (const T *)u0 : (zero ? nullptr : uA[l]);
@@ -589,7 +594,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             return 0;
         }
         const bool leaf = norm_up && leaf_rows0 > 0;
-        StreamArgs<T> a = stream_args<T>(n[l], B, leaf ? leaf_rows0 : 1);
+        StreamArgs<T> a = stream_args<T, NT>(n[l], B, leaf ? leaf_rows0 : 1);
         a.f = fL;
         a.u_in = uB[l];
         a.uc = uA[l + 1];
@@ -623,7 +628,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     int enqueue_norm_pass(const void *f, void *u, cudaStream_t s)
     {
         const bool leaf = leaf_rows0 > 0;
-        StreamArgs<T> a = stream_args<T>(n[0], B, leaf ? leaf_rows0 : 1);
+        StreamArgs<T> a = stream_args<T, NT>(n[0], B, leaf ? leaf_rows0 : 1);
         a.f = (const T *)f;
         a.u_in = (const T *)u;
         a.active = d_active;
@@ -1031,7 +1036,7 @@ int run_op(Op op, const tmg_level_desc &d, const OpArgs &x, cudaStream_t s)
 {
     const LevelC<T, NT> L = make_level<T, NT>(d);
     const long long n = d.n_slabs;
-    StreamArgs<T> a = stream_args<T>(n, x.batch, 1);
+    StreamArgs<T> a = stream_args<T, NT>(n, x.batch, 1);
     a.f = (const T *)x.f;
     a.u_in = (const T *)x.u_in;
     a.active = x.active;

@@ -17,7 +17,7 @@ template <typename T, int NT, int NU, bool SP, int KIND, int PERM>
 int launch_one(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_t s)
 {
     auto k = stream_kernel<T, NT, NU, SP, KIND, PERM>;
-    constexpr size_t smem = RowLayout<T, NT, KindProlongs<KIND>::value>::SMEM_BYTES;
+    constexpr size_t smem = RowLayout<T, NT, KindProlongs<KIND>::value, KindLeaf<KIND>::value>::SMEM_BYTES;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -79,9 +79,7 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
     return -1;
 }
 
-template <typename T, int NT> size_t stream_smem_bytes() { return RowLayout<T, NT, true>::SMEM_BYTES; }
-template <typename T, int NT> int stream_joint_rows() { return JointRows<T, NT>::value; }
-template int stream_joint_rows<TMG_T, TMG_NT>();
+template <typename T, int NT> size_t stream_smem_bytes() { return RowLayout<T, NT, true, true>::SMEM_BYTES; }
 
 template <typename T, int NT> int tail_prepare(bool sparse, size_t smem)
 {

@@ -1,35 +1,41 @@
-// Streaming level kernels: one warp walks a contiguous chunk of slabs, 32
-// slabs (one "row") at a time.  Lane l owns slab 32*row + l of the row and
-// keeps its n_t values in registers through all sweeps of the pass:
+// Streaming level kernels: one warp walks a contiguous chunk of slabs, one
+// "row" of 32*P slabs at a time.  Lane l owns the P consecutive slabs
+// P*l .. P*l+P-1 of the row (P = 2 for n_t <= 2 in fp64 and for fp32, else 1)
+// and keeps their n_t values in registers through all sweeps of the pass:
 //
 //   down:  nu1 sweeps -> residual -> restriction        (multigrid.py:274-285)
 //   up:    prolong-add -> nu2 sweeps [-> residual norm] (multigrid.py:317-327,
 //                                                         447-459)
 //
 // Jacobi reads only slab n and n-1 of the previous iterate (multigrid.py:
-// 168-180).  What slab n needs from slab n-1 at sweep k is one rotate-shuffle
-// away: lane l receives lane l-1's value and lane 0 receives lane 31's -- the
-// value the NEXT row's lane 0 will need -- so lane 0 swaps it with the carry
-// it kept from the previous row.  A chunk that does not start at slab 0 first
-// runs one "warm-up" row over the 32 slabs before it (only lanes >= k are
-// valid after k sweeps; lane 31 needs nu+1 <= 32 of them), so warps never
-// synchronise with each other: the pass is one HBM read of u, f (and u_coarse)
-// and one write of u (and f_coarse) per slab.
+// 168-180).  A lane's second slab takes its predecessor from the lane's first
+// slab; the first slab's predecessor is one rotate-shuffle away: lane l
+// receives lane l-1's last slab and lane 0 receives lane 31's -- the value the
+// NEXT row's lane 0 will need -- so lane 0 swaps it with the carry it kept
+// from the previous row.  With P = 2 a restriction pair (2i, 2i+1) and the two
+// fine slabs of a prolongation live in one lane: no shuffles there at all.
+// A chunk that does not start at slab 0 first runs one "warm-up" row over the
+// 32*P slabs before it (after k sweeps only slabs >= k of it are valid; the
+// last one needs nu+1 <= 32*P of them), so warps never synchronise with each
+// other: the pass is one HBM read of u, f (and u_coarse) and one write of u
+// (and f_coarse) per slab.
 //
-// Rows arrive two at a time in a per-warp shared-memory ring filled by the
-// TMA engine (cp.async.bulk global->shared, completion on an mbarrier, L2
+// Rows arrive in a per-warp shared-memory ring (64 slabs per stage) filled by
+// the TMA engine (cp.async.bulk global->shared, completion on an mbarrier, L2
 // evict-first); lane 0 refills a stage as soon as the warp has read it.
-// Interior rows run a specialised path (every lane valid, every slab has a
+// Interior rows run a specialised path (every slab valid, every slab has a
 // predecessor); the problem's first row and a ragged last row take the
 // general path.
 #pragma once
 #include "tmg_slab.cuh"
+#include "tmg_types.cuh"
 
 namespace tmg {
 
-constexpr int SW_WARPS = 8;   // warps per CTA
-constexpr int SW_STAGES = 4;  // ring stages per warp (3 for the up passes: larger stages)
-constexpr int SW_GROUP = 2;   // rows per stage
+constexpr int SW_WARPS = 8;         // warps per CTA
+constexpr int SW_STAGES = 4;        // max ring stages per warp
+constexpr int SW_STAGE_SLABS = 64;  // fine slabs per ring stage
+constexpr int SW_LEAF_BATCH = 4;    // numpy leaves reduced together (one per 8 lanes)
 #ifndef TMG_MINB
 #define TMG_MINB(NT) 2
 #endif
@@ -61,15 +67,15 @@ template <typename T> struct StreamArgs {
     const T *uc;
     T *fc;
     T *r_out;
-    T *halo;               // [batch][chunks][J rows][32][NT]: each chunk's last J rows of the
-                           // ORIGINAL iterate (written by down passes, read by K_UP2 warm-ups)
+    T *halo;               // [batch][chunks][32*P][NT]: each chunk's last row of the ORIGINAL
+                           // iterate (written by down passes, read by K_UP2 warm-up rows)
     double *sq_out;
     double *leaf_out;
     const int *active;
     long long n;           // fine slabs per problem
     long long chunks;      // chunks per problem
     int batch;
-    int rows_per_chunk;    // multiple of SW_GROUP and of leaf_rows
+    int rows_per_chunk;    // rows of 32*P slabs; a multiple of the stage and of leaf_rows
     int leaf_rows;         // rows per numpy pairwise leaf (SF_NORM_LEAF)
     int flags;
 };
@@ -126,35 +132,101 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-template <typename T, int NT, bool WITH_C> struct RowLayout {
-    static constexpr int ROW = 32 * NT;   // elements of one fine row
-    static constexpr int HALF = 16 * NT;  // elements of the matching coarse half-row
-    static constexpr int OFF_F = SW_GROUP * ROW;
-    static constexpr int OFF_C = 2 * SW_GROUP * ROW;
-    static constexpr int STAGE = SW_GROUP * (2 * ROW + (WITH_C ? HALF : 0));
-    // ring depth from a per-CTA budget that keeps the register-limited
-    // occupancy (3 CTAs/SM for n_t <= 2, 2 CTAs/SM above): 2..4 stages
-    static constexpr size_t BUDGET = NT <= 2 ? 72 * 1024 : 100 * 1024;
-    static constexpr int ST_RAW = (int)(BUDGET / (SW_WARPS * sizeof(T) * STAGE));
-    static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > SW_STAGES ? SW_STAGES : ST_RAW);
-    // per-warp copy of (R1, R2) for n_t >= 3 (R2 padded by 2 elements so the
-    // even and odd half-warps read different banks)
-    static constexpr int RELEMS = NT >= 3 ? 2 * NT * NT + 2 : 0;
-    static constexpr int RSTRIDE = NT * NT + 2;
-    static constexpr size_t RBYTES = ((sizeof(T) * RELEMS + 15) / 16) * 16;
-    static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * ST + RBYTES;
-    // mbarrier block (one 8-byte barrier per warp and stage), padded to 128 B
-    static constexpr size_t BAR_BYTES = ((SW_WARPS * ST * 8 + 127) / 128) * 128;
-    static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * SW_WARPS;
-};
-
 template <int KIND> struct KindProlongs {
     static constexpr bool value = KIND != K_DOWN && KIND != K_DOWNNORM;
 };
-// rows processed jointly (must agree between a level's down and up passes:
-// the halo holds J rows)
-template <typename T, int NT> struct JointRows {
-    static constexpr int value = (NT <= 2 || sizeof(T) == 4) ? 2 : 1;
+template <int KIND> struct KindLeaf {
+    static constexpr bool value = KIND == K_GENERIC || KIND == K_UPNORM || KIND == K_DOWNNORM;
+};
+
+// vector load/store of one lane's P*NT consecutive elements (16-byte pieces
+// when the lane stride allows, else 8-byte, else scalar)
+template <typename T, int NE> struct LaneVec {
+    static constexpr int BYTES = NE * (int)sizeof(T);
+    static constexpr int VB = (BYTES % 16 == 0) ? 16 : (BYTES % 8 == 0) ? 8 : (int)sizeof(T);
+    static constexpr int PER = VB / (int)sizeof(T);
+};
+template <typename T, int NE> __device__ __forceinline__ void vload(const T *p, T (&x)[NE])
+{
+    constexpr int PER = LaneVec<T, NE>::PER;
+#pragma unroll
+    for (int i = 0; i < NE; i += PER) {
+        if constexpr (sizeof(T) == 8 && PER == 2) {
+            double2 v = *reinterpret_cast<const double2 *>(p + i);
+            x[i] = v.x; x[i + 1] = v.y;
+        } else if constexpr (sizeof(T) == 4 && PER == 4) {
+            float4 v = *reinterpret_cast<const float4 *>(p + i);
+            x[i] = v.x; x[i + 1] = v.y; x[i + 2] = v.z; x[i + 3] = v.w;
+        } else if constexpr (sizeof(T) == 4 && PER == 2) {
+            float2 v = *reinterpret_cast<const float2 *>(p + i);
+            x[i] = v.x; x[i + 1] = v.y;
+        } else {
+            x[i] = p[i];
+        }
+    }
+}
+template <typename T, int NE> __device__ __forceinline__ void vstore(T *p, const T (&x)[NE])
+{
+    constexpr int PER = LaneVec<T, NE>::PER;
+#pragma unroll
+    for (int i = 0; i < NE; i += PER) {
+        if constexpr (sizeof(T) == 8 && PER == 2) {
+            *reinterpret_cast<double2 *>(p + i) = make_double2(x[i], x[i + 1]);
+        } else if constexpr (sizeof(T) == 4 && PER == 4) {
+            *reinterpret_cast<float4 *>(p + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+        } else if constexpr (sizeof(T) == 4 && PER == 2) {
+            *reinterpret_cast<float2 *>(p + i) = make_float2(x[i], x[i + 1]);
+        } else {
+            p[i] = x[i];
+        }
+    }
+}
+template <typename T, int NT, int P> __device__ __forceinline__ void load_lane(const T *p, T (&x)[P][NT])
+{
+    T v[P * NT];
+    vload<T, P * NT>(p, v);
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) x[q][i] = v[q * NT + i];
+}
+template <typename T, int NT, int P> __device__ __forceinline__ void store_lane(T *p, const T (&x)[P][NT])
+{
+    T v[P * NT];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) v[q * NT + i] = x[q][i];
+    vstore<T, P * NT>(p, v);
+}
+
+template <typename T, int NT, bool WITH_C, bool LEAF> struct RowLayout {
+    static constexpr int P = slabs_per_lane<T, NT>();
+    static constexpr int W = 32 * P;                // slabs per row
+    static constexpr int G = SW_STAGE_SLABS / W;    // rows per ring stage
+    static constexpr int ROW = W * NT;              // elements of one fine row
+    static constexpr int HALF = ROW / 2;            // elements of the matching coarse half-row
+    static constexpr int OFF_F = G * ROW;
+    static constexpr int OFF_C = 2 * G * ROW;
+    static constexpr int STAGE = G * (2 * ROW + (WITH_C ? HALF : 0));
+    // per-warp numpy leaf buffer: LB leaves of <= 128 slab norms each
+    static constexpr int LB = P == 2 ? SW_LEAF_BATCH : 2;
+    static constexpr int LEAFBUF = LEAF ? LB * 128 : 0;
+    static constexpr size_t LBYTES = sizeof(T) * LEAFBUF;
+    // per-warp copy of (R1, R2) for n_t >= 3 with one slab per lane (R2 padded
+    // by 2 elements so the even and odd half-warps read different banks)
+    static constexpr int RELEMS = (P == 1 && NT >= 3) ? 2 * NT * NT + 2 : 0;
+    static constexpr int RSTRIDE = NT * NT + 2;
+    static constexpr size_t RBYTES = ((sizeof(T) * RELEMS + 15) / 16) * 16;
+    // ring depth from a per-CTA budget that keeps 2 CTAs/SM: 2..4 stages
+    static constexpr size_t CAP = NT <= 2 ? 104 * 1024 : 110 * 1024;
+    static constexpr size_t WARP_CAP = CAP / SW_WARPS - LBYTES - RBYTES;
+    static constexpr int ST_RAW = (int)(WARP_CAP / (sizeof(T) * STAGE));
+    static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > SW_STAGES ? SW_STAGES : ST_RAW);
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * ST + RBYTES + LBYTES;
+    // mbarrier block (one 8-byte barrier per warp and stage), padded to 128 B
+    static constexpr size_t BAR_BYTES = ((SW_WARPS * ST * 8 + 127) / 128) * 128;
+    static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * SW_WARPS;
 };
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct Streamer {
@@ -169,23 +241,25 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     static constexpr int NPRE = KIND == K_UP2 ? NU : 0;
     // norm of the pass's input (K_DOWNNORM) rather than of its output
     static constexpr bool NORM_IN = KIND == K_DOWNNORM && NU > 0;
-    // rows swept jointly per lane (two dependency chains hide fp64 latency);
-    // larger blocks have enough independent work per row already
-    static constexpr int J = JointRows<T, NT>::value;
+    static constexpr int P = slabs_per_lane<T, NT>();
+    static constexpr int W = 32 * P;
+    static constexpr int LB = RowLayout<T, NT, true, true>::LB;
     const LevelC<T, NT> &L;
     const StreamArgs<T> &a;
     int lane;
     int flags;
-    // this lane's transfer block (odd lanes R2, even lanes R1): registers for
-    // n_t <= 2, a per-warp shared-memory copy for larger blocks
-    static constexpr bool RREG = NT * NT * sizeof(T) <= 64;
+    // one slab per lane: this lane's transfer block (odd lanes R2, even lanes
+    // R1) in registers for n_t <= 2, a per-warp shared-memory copy above
+    static constexpr bool RREG = P == 1 && NT * NT * sizeof(T) <= 64;
     T Rm[RREG ? NT * NT : 1];
     const T *Rs;
     C carry[NPRE + NU + 1];  // lane 0: predecessor data of the next row, per sweep
-    T leaf_acc;
-    int leaf_q;         // row position inside the current numpy leaf
+    T *leafbuf;              // per-warp numpy leaf buffer (SF_NORM_LEAF)
+    int leaf_q;              // rows buffered in leafbuf
+    long long leaf0;         // index of the first buffered leaf
     long long nc;
-    bool write_u;       // the pass stores u (u_out given)
+    bool write_u;            // the pass stores u (u_out given)
+    bool vec_out;            // u_out rows are 16-byte aligned (vector stores)
 
     __device__ __forceinline__ bool has(int f) const
     {
@@ -196,170 +270,180 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         return has(SF_RESTRICT) || has(SF_NORM_LEAF) || has(SF_NORM_SQ) || has(SF_WRITE_R);
     }
 
-    // numpy pairwise leaf (np.sum, multigrid.py:459): accumulator j sums leaf
-    // elements j, j+8, j+16, ... in order; 8 accumulators combined as
-    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) at the leaf's last row
-    __device__ __forceinline__ void leaf_add(const T (&r)[NT], long long row, int b)
+    // numpy pairwise leaves (np.sum over the slab norms, multigrid.py:459):
+    // accumulator j of a leaf sums its slabs j, j+8, j+16, ... in order; the
+    // 8 accumulators combine as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)).  Slab
+    // norms go to shared memory; every LB leaves, lane 8l+j runs accumulator
+    // j of leaf l (a 16-term sequential sum) and 3 shuffle steps combine them.
+    __device__ __forceinline__ void leaf_flush(int b)
     {
-        T sq = sqnorm<T, NT>(r);
-        T v1 = __shfl_down_sync(0xffffffffu, sq, 8);
-        T v2 = __shfl_down_sync(0xffffffffu, sq, 16);
-        T v3 = __shfl_down_sync(0xffffffffu, sq, 24);
-        leaf_acc = (leaf_q == 0) ? sq : FP<T>::add(leaf_acc, sq);
-        leaf_acc = FP<T>::add(leaf_acc, v1);
-        leaf_acc = FP<T>::add(leaf_acc, v2);
-        leaf_acc = FP<T>::add(leaf_acc, v3);
-        if (leaf_q == a.leaf_rows - 1) {
-            T t1 = FP<T>::add(leaf_acc, __shfl_down_sync(0xffffffffu, leaf_acc, 1));
-            T t2 = FP<T>::add(t1, __shfl_down_sync(0xffffffffu, t1, 2));
-            T t3 = FP<T>::add(t2, __shfl_down_sync(0xffffffffu, t2, 4));
-            const long long nleaves = a.n / (32LL * a.leaf_rows);
-            if (lane == 0) a.leaf_out[(size_t)b * nleaves + row / a.leaf_rows] = (double)t3;
-            leaf_q = 0;
-        } else {
-            leaf_q += 1;
+        __syncwarp();
+        const int nl = leaf_q / a.leaf_rows;
+        const int m = a.leaf_rows * W;
+        const int l = lane >> 3, j = lane & 7;
+        T acc = T(0);
+        if (l < nl) {
+            const T *p = leafbuf + l * m + j;
+            acc = p[0];
+            for (int i = 8; i < m; i += 8) acc = FP<T>::add(acc, p[i]);
         }
+        T t1 = FP<T>::add(acc, __shfl_down_sync(0xffffffffu, acc, 1));
+        T t2 = FP<T>::add(t1, __shfl_down_sync(0xffffffffu, t1, 2));
+        T t3 = FP<T>::add(t2, __shfl_down_sync(0xffffffffu, t2, 4));
+        const long long nleaves = a.n / ((long long)W * a.leaf_rows);
+        if (j == 0 && l < nl) a.leaf_out[(size_t)b * nleaves + leaf0 + l] = (double)t3;
+        __syncwarp();
+        leaf_q = 0;
+    }
+    __device__ __forceinline__ void leaf_row(const T (&r)[P][NT], long long row, int b)
+    {
+        if (leaf_q == 0) leaf0 = row / a.leaf_rows;
+        T sq[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) sq[q] = sqnorm<T, NT>(r[q]);
+        vstore<T, P>(leafbuf + leaf_q * W + lane * P, sq);
+        if (++leaf_q == LB * a.leaf_rows) leaf_flush(b);
     }
 
-    // predecessor data for JJ consecutive rows at sweep k (rotate-shuffle + carry)
-    template <int JJ>
-    __device__ __forceinline__ void exchange(const T (&u)[JJ][NT], int k, C (&prev)[JJ])
+    // predecessor data of the row's P slabs at sweep k: the lane's own earlier
+    // slab, or (first slab) lane-1's last slab / the carry from the previous row
+    __device__ __forceinline__ void exchange(const T (&u)[P][NT], int k, C (&prev)[P])
     {
-        C x[JJ];
+        C own[P];
 #pragma unroll
-        for (int q = 0; q < JJ; ++q) {
-            C own = make_cpl<T, NT, SPARSE>(L, u[q]);
-            x[q] = cpl_shfl<T, NT, SPARSE>(own, (lane + 31) & 31);
-        }
-        prev[0] = x[0];
+        for (int q = 0; q < P; ++q) own[q] = make_cpl<T, NT, SPARSE>(L, u[q]);
+        C x = cpl_shfl<T, NT, SPARSE>(own[P - 1], (lane + 31) & 31);
+        prev[0] = x;
         cpl_select<T, NT, SPARSE>(prev[0], carry[k], lane == 0);
 #pragma unroll
-        for (int q = 1; q < JJ; ++q) {
-            prev[q] = x[q];
-            cpl_select<T, NT, SPARSE>(prev[q], x[q - 1], lane == 0);
-        }
-        carry[k] = x[JJ - 1];
+        for (int q = 1; q < P; ++q) prev[q] = own[q - 1];
+        carry[k] = x;
     }
 
-    // JJ rows starting at slab0 (this lane's slab in the first row);
-    // INTERIOR: every slab exists and none is slab 0 of the problem.
-    // Rows q >= nrow are beyond the chunk: computed but never stored.
-    // uo/fco: this lane's u_out / f_coarse element for the first row (row
-    // stride 32*NT / 16*NT elements), advanced by the caller
-    template <bool INTERIOR, int JJ>
-    __device__ __forceinline__ void rows(T (&u)[JJ][NT], const T (&f)[JJ][NT], const T (&uc)[JJ][NT],
-                                         long long slab0, long long row_idx0, int nrow, bool warm, int b,
-                                         T *uo, T *fco, bool zg)
+    // one row; slab0 = this lane's first slab.  INTERIOR: every slab exists
+    // and none is slab 0 of the problem.  uo / fco: this lane's u_out /
+    // f_coarse elements of the row.
+    template <bool INTERIOR>
+    __device__ __forceinline__ void row(T (&u)[P][NT], const T (&f)[P][NT], const T (&uc)[NT], long long slab0,
+                                        long long row_idx, bool warm, int b, T *uo, T *fco, bool zg)
     {
-        bool valid[JJ], hp[JJ];
+        bool valid[P], hp[P];
 #pragma unroll
-        for (int q = 0; q < JJ; ++q) {
-            const long long sl = slab0 + 32 * q;
-            valid[q] = INTERIOR || (q < nrow && sl < a.n);
-            hp[q] = INTERIOR || sl > 0;
+        for (int q = 0; q < P; ++q) {
+            valid[q] = INTERIOR || slab0 + q < a.n;
+            hp[q] = INTERIOR || slab0 + q > 0;
         }
         // K_UP2: the down pass's pre-sweeps, recomputed (same bits)
 #pragma unroll
         for (int k = 0; k < NPRE; ++k) {
             if (k == 0 && zg) {
-                sweep_zero_j<T, NT, PERM, JJ>(L, u, f);
+                sweep_zero_j<T, NT, PERM, P>(L, u, f);
                 continue;
             }
-            C prev[JJ];
-            exchange<JJ>(u, k, prev);
-            sweep_j<T, NT, SPARSE, PERM, JJ>(L, u, f, prev, hp);
+            C prev[P];
+            exchange(u, k, prev);
+            sweep_j<T, NT, SPARSE, PERM, P>(L, u, f, prev, hp);
         }
+        if (has(SF_PROLONG)) {
 #pragma unroll
-        for (int q = 0; q < JJ; ++q) {
-            const long long sl = slab0 + 32 * q;
-            if (has(SF_PROLONG)) {
-                if (INTERIOR || sl < 2 * nc) {
-                    if constexpr (RREG) prolong_reg<T, NT>(Rm, uc[q], u[q]);
-                    else prolong_ptr<T, NT>(Rs, uc[q], u[q]);
+            for (int q = 0; q < P; ++q) {
+                if (INTERIOR || slab0 + q < 2 * nc) {
+                    if constexpr (P == 2) {
+                        if (q == 0) prolong_reg<T, NT>(L.R1, uc, u[q]);
+                        else prolong_reg<T, NT>(L.R2, uc, u[q]);
+                    } else if constexpr (RREG) prolong_reg<T, NT>(Rm, uc, u[q]);
+                    else prolong_ptr<T, NT>(Rs, uc, u[q]);
                 }
             }
         }
 #pragma unroll
         for (int k = 0; k < NU; ++k) {
             if (!NORM_IN && NPRE == 0 && k == 0 && zg) {
-                sweep_zero_j<T, NT, PERM, JJ>(L, u, f);
+                sweep_zero_j<T, NT, PERM, P>(L, u, f);
                 continue;
             }
-            C prev[JJ];
-            exchange<JJ>(u, NPRE + k, prev);
+            C prev[P];
+            exchange(u, NPRE + k, prev);
             if (NORM_IN && k == 0) {
                 // the first sweep's residual IS the input's residual: take its norm
-                T y[JJ][NT];
+                T y[P][NT];
 #pragma unroll
-                for (int q = 0; q < JJ; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], prev[q], hp[q], y[q]);
+                for (int q = 0; q < P; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], prev[q], hp[q], y[q]);
                 if (!warm) {
+                    T r[P][NT];
 #pragma unroll
-                    for (int q = 0; q < JJ; ++q) {
-                        if (INTERIOR || q < nrow) {
-                            T r[NT];
-                            unpermute<T, NT, PERM>(L, y[q], r);
-                            leaf_add(r, row_idx0 + q, b);
-                        }
-                    }
+                    for (int q = 0; q < P; ++q) unpermute<T, NT, PERM>(L, y[q], r[q]);
+                    leaf_row(r, row_idx, b);
                 }
-                finish_j<T, NT, JJ>(L, u, y);
+                finish_j<T, NT, P>(L, u, y);
             } else {
-                sweep_j<T, NT, SPARSE, PERM, JJ>(L, u, f, prev, hp);
+                sweep_j<T, NT, SPARSE, PERM, P>(L, u, f, prev, hp);
             }
         }
         if (need_r()) {
-            C prev[JJ];
-            exchange<JJ>(u, NPRE + NU, prev);
+            C prev[P];
+            exchange(u, NPRE + NU, prev);
             if (!warm) {
+                T r[P][NT];
 #pragma unroll
-                for (int q = 0; q < JJ; ++q) {
-                    const long long sl = slab0 + 32 * q;
-                    T r[NT];
-                    residual<T, NT, SPARSE>(L, u[q], f[q], prev[q], hp[q], r);
-                    if (has(SF_WRITE_R) && valid[q]) store_slab<T, NT>(a.r_out + ((size_t)b * a.n + sl) * NT, r);
-                    if (has(SF_RESTRICT)) {
-                        T p[NT], qq[NT];
-                        if constexpr (RREG) restrict_reg<T, NT>(Rm, r, p);
-                        else restrict_ptr<T, NT>(Rs, r, p);
+                for (int q = 0; q < P; ++q) residual<T, NT, SPARSE>(L, u[q], f[q], prev[q], hp[q], r[q]);
+                if (has(SF_WRITE_R)) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (valid[q]) store_slab<T, NT>(a.r_out + ((size_t)b * a.n + slab0 + q) * NT, r[q]);
+                }
+                if (has(SF_RESTRICT)) {
+                    T p[NT];
+                    bool st;
+                    if constexpr (P == 2) {
+                        T p1[NT];
+                        restrict_reg<T, NT>(L.R1, r[0], p);
+                        restrict_reg<T, NT>(L.R2, r[1], p1);
+#pragma unroll
+                        for (int i = 0; i < NT; ++i) p[i] = FP<T>::add(p[i], p1[i]);
+                        st = true;
+                    } else {
+                        T qq[NT];
+                        if constexpr (RREG) restrict_reg<T, NT>(Rm, r[0], p);
+                        else restrict_ptr<T, NT>(Rs, r[0], p);
 #pragma unroll
                         for (int i = 0; i < NT; ++i) qq[i] = __shfl_down_sync(0xffffffffu, p[i], 1);
 #pragma unroll
                         for (int i = 0; i < NT; ++i) p[i] = FP<T>::add(p[i], qq[i]);
-                        const long long cidx = sl >> 1;
-                        if (!(lane & 1) && (INTERIOR || (valid[q] && cidx < nc)))
-                            store_slab<T, NT>(fco + q * 16 * NT, p);
+                        st = !(lane & 1);
                     }
-                    if (has(SF_NORM_SQ)) {
-                        if (valid[q]) a.sq_out[(size_t)b * a.n + sl] = (double)sqnorm<T, NT>(r);
-                    }
-                    if (!NORM_IN && has(SF_NORM_LEAF) && (INTERIOR || q < nrow)) leaf_add(r, row_idx0 + q, b);
+                    if (st && (INTERIOR || (slab0 >> 1) < nc)) store_slab<T, NT>(fco, p);
                 }
+                if (has(SF_NORM_SQ)) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (valid[q]) a.sq_out[(size_t)b * a.n + slab0 + q] = (double)sqnorm<T, NT>(r[q]);
+                }
+                if (!NORM_IN && has(SF_NORM_LEAF)) leaf_row(r, row_idx, b);
             }
         }
         if (has(SF_WRITE_U) && !warm && write_u) {
+            if (INTERIOR && vec_out) {
+                store_lane<T, NT, P>(uo, u);
+            } else {
 #pragma unroll
-            for (int q = 0; q < JJ; ++q)
-                if (valid[q]) store_slab<T, NT>(uo + q * 32 * NT, u[q]);
+                for (int q = 0; q < P; ++q)
+                    if (valid[q]) store_slab<T, NT>(uo + q * NT, u[q]);
+            }
         }
     }
 };
-
-template <typename T, int NT>
-__device__ __forceinline__ void load_row(const T *src, T (&x)[NT], bool vec)
-{
-    if (vec) load_slab<T, NT>(src, x);
-    else load_slab_scalar<T, NT>(src, x);
-}
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM>
 __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     stream_kernel(const __grid_constant__ LevelC<T, NT> L, const __grid_constant__ StreamArgs<T> a)
 {
     constexpr bool WITH_C = KindProlongs<KIND>::value;
-    using Lay = RowLayout<T, NT, WITH_C>;
+    using Lay = RowLayout<T, NT, WITH_C, KindLeaf<KIND>::value>;
     using S = Streamer<T, NT, NU, SPARSE, KIND, PERM>;
-    constexpr int J = S::J;
-    constexpr int G = SW_GROUP;
+    constexpr int P = S::P;
+    constexpr int W = Lay::W;
+    constexpr int G = Lay::G;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -372,13 +456,14 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     S st{L, a, lane, a.flags};
     const long long n = a.n;
     st.nc = n >> 1;
-    const long long nrows = (n + 31) >> 5;
+    const long long nrows = (n + W - 1) / W;
     const long long row0 = chunk * a.rows_per_chunk;
     const int rows = (int)min((long long)a.rows_per_chunk, nrows - row0);
     const int ngroups = (rows + G - 1) / G;
     const bool zero_guess = a.flags & SF_ZERO_GUESS;
     const bool tma = a.flags & SF_TMA;
     const bool prolong = WITH_C && st.has(SF_PROLONG);
+    const int lofs = lane * P;  // this lane's first slab within a row
 
     const T *fb = a.f + (size_t)b * n * NT;
     const T *ub = zero_guess ? nullptr : a.u_in + (size_t)b * n * NT;
@@ -387,36 +472,40 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     constexpr int ST = Lay::ST;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * ST;
     unsigned char *wbase = smem + Lay::BAR_BYTES + (size_t)warp * Lay::BYTES_PER_WARP;
-    T *ring = reinterpret_cast<T *>(wbase + Lay::RBYTES);
-    if (st.has(SF_RESTRICT) || prolong) {
-        const bool odd = lane & 1;
-        if constexpr (S::RREG) {
+    T *ring = reinterpret_cast<T *>(wbase + Lay::RBYTES + Lay::LBYTES);
+    st.leafbuf = reinterpret_cast<T *>(wbase + Lay::RBYTES);
+    if constexpr (P == 1) {
+        if (st.has(SF_RESTRICT) || prolong) {
+            const bool odd = lane & 1;
+            if constexpr (S::RREG) {
 #pragma unroll
-            for (int i = 0; i < NT * NT; ++i) st.Rm[i] = odd ? L.R2[i] : L.R1[i];
-        } else {
-            T *rs = reinterpret_cast<T *>(wbase);
-            for (int i = lane; i < NT * NT; i += 32) {
-                rs[i] = L.R1[i];
-                rs[Lay::RSTRIDE + i] = L.R2[i];
+                for (int i = 0; i < NT * NT; ++i) st.Rm[i] = odd ? L.R2[i] : L.R1[i];
+            } else {
+                T *rs = reinterpret_cast<T *>(wbase);
+                for (int i = lane; i < NT * NT; i += 32) {
+                    rs[i] = L.R1[i];
+                    rs[Lay::RSTRIDE + i] = L.R2[i];
+                }
+                __syncwarp();
+                st.Rs = rs + (odd ? Lay::RSTRIDE : 0);
             }
-            __syncwarp();
-            st.Rs = rs + (odd ? Lay::RSTRIDE : 0);
         }
     }
 #pragma unroll
     for (int k = 0; k <= S::NPRE + NU; ++k) cpl_zero(st.carry[k]);
-    st.leaf_acc = T(0);
     st.leaf_q = 0;
+    st.leaf0 = 0;
 
     // groups [0, g_full) consist of G whole rows (and go through the ring when
     // TMA is on); groups [g_int0, g_full) are interior (no slab 0, all valid)
-    const int g_full = (int)max(0LL, min((long long)(rows / G), (n / 32 - row0) / G));
+    const int g_full = (int)max(0LL, min((long long)(rows / G), (n / W - row0) / G));
     const int g_int0 = row0 == 0 ? 1 : 0;
     auto group_tma = [&](int g) -> bool { return tma && g < g_full; };
-    // per-lane output cursors (advanced by G rows per group)
+    // per-lane output cursors (advanced by one row at a time)
     st.write_u = st.has(SF_WRITE_U) && a.u_out != nullptr;
-    T *uo = st.write_u ? a.u_out + ((size_t)b * n + (size_t)row0 * 32 + lane) * NT : nullptr;
-    T *fco = st.has(SF_RESTRICT) ? a.fc + ((size_t)b * st.nc + (size_t)row0 * 16 + (lane >> 1)) * NT : nullptr;
+    st.vec_out = st.write_u && (((uintptr_t)a.u_out & 15) == 0) && (((n * NT * sizeof(T)) & 15) == 0);
+    T *uo = st.write_u ? a.u_out + ((size_t)b * n + (size_t)row0 * W + lofs) * NT : nullptr;
+    T *fco = st.has(SF_RESTRICT) ? a.fc + ((size_t)b * st.nc + (((size_t)row0 * W + lofs) >> 1)) * NT : nullptr;
     uint64_t pol = 0;
     if (lane == 0 && tma) {
 #pragma unroll
@@ -429,7 +518,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
         if (!group_tma(g)) return;
         T *stg = ring + (size_t)(g % ST) * Lay::STAGE;
         uint64_t *bar = &bars[g % ST];
-        const long long s0 = (row0 + (long long)g * G) * 32;
+        const long long s0 = (row0 + (long long)g * G) * W;
         const uint32_t bytes = (uint32_t)(G * Lay::ROW * sizeof(T));
         const uint32_t cbytes = prolong ? (uint32_t)(G * Lay::HALF * sizeof(T)) : 0u;
         mbar_expect_tx(bar, bytes * (zero_guess ? 1u : 2u) + cbytes);
@@ -440,87 +529,76 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     if (lane == 0 && tma)
         for (int g = 0; g < ngroups && g < ST; ++g) issue(g);
 
-    // warm-up: the J rows before the chunk, for the carries only
-    if (row0 > 0) {
-        T u[J][NT], f[J][NT], uc[J][NT];
-        const long long wr0 = row0 - J;
+    // general (bounds-checked) load of one row
+    auto load_row_gen = [&](long long r, T (&u)[P][NT], T (&f)[P][NT], T (&uc)[NT], bool with_u) {
+        const long long s0 = r * W + lofs;
 #pragma unroll
-        for (int q = 0; q < J; ++q) {
-            const long long sl = (wr0 + q) * 32 + lane;
+        for (int q = 0; q < P; ++q) {
             zero_slab<T, NT>(u[q]);
-            zero_slab<T, NT>(uc[q]);
-            load_row<T, NT>(fb + sl * NT, f[q], tma);
-            if (!zero_guess) {
-                if (S::NPRE > 0)  // the neighbour chunk may already have overwritten these rows
-                    load_row<T, NT>(a.halo + (((size_t)b * a.chunks + chunk - 1) * J + q) * 32 * NT + lane * NT,
-                                    u[q], tma);
-                else
-                    load_row<T, NT>(ub + sl * NT, u[q], tma);
+            zero_slab<T, NT>(f[q]);
+            if (s0 + q < n) {
+                load_slab_scalar<T, NT>(fb + (s0 + q) * NT, f[q]);
+                if (with_u) load_slab_scalar<T, NT>(ub + (s0 + q) * NT, u[q]);
             }
-            if (prolong) load_row<T, NT>(ucb + (sl >> 1) * NT, uc[q], tma);
         }
-        if (wr0 > 0) st.template rows<true, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr, zero_guess);
-        else st.template rows<false, J>(u, f, uc, wr0 * 32 + lane, wr0, J, true, b, nullptr, nullptr, zero_guess);
+        zero_slab<T, NT>(uc);
+        if (prolong && (s0 >> 1) < st.nc) load_slab_scalar<T, NT>(ucb + (s0 >> 1) * NT, uc);
+    };
+
+    // warm-up: the row before the chunk, for the carries only
+    if (row0 > 0) {
+        T u[P][NT], f[P][NT], uc[NT];
+        const long long wr = row0 - 1;
+        load_row_gen(wr, u, f, uc, !zero_guess && S::NPRE == 0);
+        if (S::NPRE > 0 && !zero_guess)  // the neighbour chunk may already have overwritten this row
+            load_lane<T, NT, P>(a.halo + ((size_t)b * a.chunks + chunk - 1) * Lay::ROW + lofs * NT, u);
+        if (wr > 0) st.template row<true>(u, f, uc, wr * W + lofs, wr, true, b, nullptr, nullptr, zero_guess);
+        else st.template row<false>(u, f, uc, wr * W + lofs, wr, true, b, nullptr, nullptr, zero_guess);
     }
 
+    const bool halo_out = a.halo && !zero_guess && chunk + 1 < a.chunks && !S::NPRE;
     for (int g = 0; g < ngroups; ++g) {
         const bool gt = group_tma(g);
         const T *stg = ring + (size_t)(g % ST) * Lay::STAGE;
-        const long long r0g = row0 + (long long)g * G;
-        const int nrow = min(G, rows - g * G);
         const bool interior = g >= g_int0 && g < g_full;
         if (gt) mbar_wait(&bars[g % ST], (uint32_t)((g / ST) & 1));
 #pragma unroll
-        for (int q0 = 0; q0 < G; q0 += J) {
-            T u[J][NT], f[J][NT], uc[J][NT];
+        for (int qq = 0; qq < G; ++qq) {
+            const int rr = g * G + qq;  // row within the chunk
+            if (G > 1 && rr >= rows) break;
+            const long long ridx = row0 + rr;
+            T u[P][NT], f[P][NT], uc[NT];
+            if (gt) {
+                load_lane<T, NT, P>(stg + Lay::OFF_F + qq * Lay::ROW + lofs * NT, f);
+                if (zero_guess) {
 #pragma unroll
-            for (int q = 0; q < J; ++q) {
-                const int qq = q0 + q;
-                const long long sl = (r0g + qq) * 32 + lane;
-                if (gt) {
-                    load_slab<T, NT>(stg + Lay::OFF_F + qq * Lay::ROW + lane * NT, f[q]);
-                    if (zero_guess) zero_slab<T, NT>(u[q]);
-                    else load_slab<T, NT>(stg + qq * Lay::ROW + lane * NT, u[q]);
-                    if (prolong) load_slab<T, NT>(stg + Lay::OFF_C + qq * Lay::HALF + (lane >> 1) * NT, uc[q]);
-                    else zero_slab<T, NT>(uc[q]);
+                    for (int q = 0; q < P; ++q) zero_slab<T, NT>(u[q]);
                 } else {
-                    zero_slab<T, NT>(u[q]);
-                    zero_slab<T, NT>(f[q]);
-                    zero_slab<T, NT>(uc[q]);
-                    if (qq < nrow && sl < n) {
-                        load_slab_scalar<T, NT>(fb + sl * NT, f[q]);
-                        if (!zero_guess) load_slab_scalar<T, NT>(ub + sl * NT, u[q]);
-                        if (prolong && sl < 2 * st.nc) load_slab_scalar<T, NT>(ucb + (sl >> 1) * NT, uc[q]);
-                    }
+                    load_lane<T, NT, P>(stg + qq * Lay::ROW + lofs * NT, u);
                 }
-            }
-            if (a.halo && !zero_guess && chunk + 1 < a.chunks && !S::NPRE) {
-                // last J rows of the chunk: the next chunk's up-pass warm-up input
-#pragma unroll
-                for (int q = 0; q < J; ++q) {
-                    const int rr = g * G + q0 + q;
-                    if (rr >= rows - J && rr < rows)
-                        store_slab<T, NT>(a.halo + (((size_t)b * a.chunks + chunk) * J + (rr - (rows - J))) * 32 * NT +
-                                              lane * NT, u[q]);
+                if (prolong) load_slab<T, NT>(stg + Lay::OFF_C + qq * Lay::HALF + (lofs >> 1) * NT, uc);
+                else zero_slab<T, NT>(uc);
+                if (qq == G - 1) {
+                    // the stage is fully read: hand it back to the copy engine
+                    __syncwarp();
+                    if (lane == 0 && g + ST < ngroups) issue(g + ST);
                 }
+            } else {
+                load_row_gen(ridx, u, f, uc, !zero_guess);
             }
-            if (q0 + J >= G) {
-                // the stage is fully read: hand it back to the copy engine
-                __syncwarp();
-                if (gt && lane == 0 && g + ST < ngroups) issue(g + ST);
+            if (halo_out && rr == rows - 1) {
+                // the chunk's last row: the next chunk's up-pass warm-up input
+                store_lane<T, NT, P>(a.halo + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT, u);
             }
-            if (q0 < nrow) {
-                if (interior)
-                    st.template rows<true, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, J, false, b, uo, fco,
-                                              zero_guess);
-                else
-                    st.template rows<false, J>(u, f, uc, (r0g + q0) * 32 + lane, r0g + q0, nrow - q0, false, b,
-                                               uo, fco, zero_guess);
-            }
-            if (st.write_u) uo += J * 32 * NT;
-            if (fco) fco += J * 16 * NT;
+            if (interior)
+                st.template row<true>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, zero_guess);
+            else
+                st.template row<false>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, zero_guess);
+            if (st.write_u) uo += Lay::ROW;
+            if (fco) fco += Lay::HALF;
         }
     }
+    if (KindLeaf<KIND>::value && st.has(SF_NORM_LEAF) && st.leaf_q > 0) st.leaf_flush(b);
 }
 
 }  // namespace tmg

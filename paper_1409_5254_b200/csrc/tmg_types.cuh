@@ -7,6 +7,11 @@ namespace tmg {
 constexpr int TAIL_THREADS = 512;
 constexpr int MAXLEV = 48;
 
+// streaming kernels: consecutive slabs owned by one lane (a row is 32*P slabs).
+// Two slabs give each lane two independent dependency chains and make the
+// restriction pairs lane-local; larger fp64 blocks would spill.
+template <typename T, int NT> constexpr int slabs_per_lane() { return (NT <= 2 || sizeof(T) == 4) ? 2 : 1; }
+
 // per-problem iteration state (multigrid.py:481-496)
 struct ProbState {
     double tol;

@@ -80,7 +80,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     def compile_unit(unit):
         name, src, defs = unit
         obj = os.path.join(objdir, name + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", *defs, "-I", INCLUDE, "-I", CSRC, "-o", obj,
+        extra = os.environ.get("TMG_NVCC_EXTRA", "").split()  # experiments: e.g. -DTMG_P2_WARPS=8
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", *defs, "-I", INCLUDE, "-I", CSRC, "-o", obj,
                os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd), flush=True)

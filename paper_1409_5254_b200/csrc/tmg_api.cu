@@ -485,6 +485,15 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             CK(cudaMalloc(&leaves, sizeof(double) * nleaves * B));
         }
         CK(cudaMalloc(&sqbuf, sizeof(double) * n[0] * B));
+        if (getenv("TMG_POISON")) {
+            // debug: NaN-fill every scratch buffer so a read-before-write shows
+            for (int l = 0; l < tl; ++l)
+                if (halo[l]) {
+                    StreamArgs<T> a = level_args(l);
+                    CK(cudaMemset(halo[l], 0xff, sizeof(T) * (size_t)B * a.chunks * ROWW * NT));
+                }
+            if (leaves) CK(cudaMemset(leaves, 0xff, sizeof(double) * nleaves * B));
+        }
         CK(cudaMalloc(&d_st, sizeof(ProbState) * B));
         CK(cudaMalloc(&d_floor, sizeof(double) * B));
         CK(cudaMalloc(&d_active, sizeof(int) * B));

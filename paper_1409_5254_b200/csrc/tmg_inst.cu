@@ -25,9 +25,10 @@ int launch_one(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_t s)
         attr = true;
     }
     const long long warps = (long long)a.batch * a.chunks;
-    const long long grid = (warps + SW_WARPS - 1) / SW_WARPS;
+    constexpr int WARPS = CtaShape<T, NT>::WARPS;
+    const long long grid = (warps + WARPS - 1) / WARPS;
     if (grid <= 0) return 0;
-    k<<<(unsigned)grid, SW_WARPS * 32, smem, s>>>(L, a);
+    k<<<(unsigned)grid, WARPS * 32, smem, s>>>(L, a);
     return (int)cudaGetLastError();
 }
 

@@ -32,13 +32,26 @@
 
 namespace tmg {
 
-constexpr int SW_WARPS = 8;         // warps per CTA
 constexpr int SW_STAGES = 4;        // max ring stages per warp
 constexpr int SW_STAGE_SLABS = 64;  // fine slabs per ring stage
 constexpr int SW_LEAF_BATCH = 4;    // numpy leaves reduced together (one per 8 lanes)
-#ifndef TMG_MINB
-#define TMG_MINB(NT) 2
+#ifndef TMG_P2_WARPS
+#define TMG_P2_WARPS 8
 #endif
+#ifndef TMG_P2_MINB
+#define TMG_P2_MINB 2
+#endif
+// CTA shape: 2 CTAs of 8 warps per SM (~110 registers per thread).  3 CTAs of
+// 6 warps (96 registers) measured no faster: the passes are issue-bound, not
+// latency-bound, at this occupancy.
+template <typename T, int NT> struct CtaShape {
+    static constexpr bool PAIR = slabs_per_lane<T, NT>() == 2;
+    static constexpr int WARPS = PAIR ? TMG_P2_WARPS : 8;
+    static constexpr int MINB = PAIR ? TMG_P2_MINB : 2;
+    // shared memory per CTA that keeps MINB CTAs resident (227 KB per SM,
+    // 1 KB reserved per CTA)
+    static constexpr size_t CAP = PAIR ? (TMG_P2_MINB >= 3 ? 72 * 1024 : 104 * 1024) : 110 * 1024;
+};
 
 enum StreamFlags : int {
     SF_ZERO_GUESS = 1,   // u_in is the zero vector: not read
@@ -115,6 +128,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     while (!mbar_try_wait(bar, parity)) {
     }
+}
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first()
 {
@@ -218,15 +235,15 @@ template <typename T, int NT, bool WITH_C, bool LEAF> struct RowLayout {
     static constexpr int RELEMS = (P == 1 && NT >= 3) ? 2 * NT * NT + 2 : 0;
     static constexpr int RSTRIDE = NT * NT + 2;
     static constexpr size_t RBYTES = ((sizeof(T) * RELEMS + 15) / 16) * 16;
-    // ring depth from a per-CTA budget that keeps 2 CTAs/SM: 2..4 stages
-    static constexpr size_t CAP = NT <= 2 ? 104 * 1024 : 110 * 1024;
-    static constexpr size_t WARP_CAP = CAP / SW_WARPS - LBYTES - RBYTES;
+    // ring depth from the per-CTA budget of the CTA shape: 2..4 stages
+    static constexpr int WARPS = CtaShape<T, NT>::WARPS;
+    static constexpr size_t WARP_CAP = CtaShape<T, NT>::CAP / WARPS - LBYTES - RBYTES;
     static constexpr int ST_RAW = (int)(WARP_CAP / (sizeof(T) * STAGE));
     static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > SW_STAGES ? SW_STAGES : ST_RAW);
     static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * ST + RBYTES + LBYTES;
     // mbarrier block (one 8-byte barrier per warp and stage), padded to 128 B
-    static constexpr size_t BAR_BYTES = ((SW_WARPS * ST * 8 + 127) / 128) * 128;
-    static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * SW_WARPS;
+    static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
+    static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
 };
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct Streamer {
@@ -435,7 +452,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
 };
 
 template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM>
-__global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
+__global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::MINB)
     stream_kernel(const __grid_constant__ LevelC<T, NT> L, const __grid_constant__ StreamArgs<T> a)
 {
     constexpr bool WITH_C = KindProlongs<KIND>::value;
@@ -447,7 +464,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const long long gw = (long long)blockIdx.x * SW_WARPS + warp;
+    const long long gw = (long long)blockIdx.x * Lay::WARPS + warp;
     if (gw >= (long long)a.batch * a.chunks) return;
     const int b = (int)(gw / a.chunks);
     const long long chunk = gw - (long long)b * a.chunks;
@@ -579,7 +596,10 @@ __global__ void __launch_bounds__(SW_WARPS * 32, TMG_MINB(NT))
                 if (prolong) load_slab<T, NT>(stg + Lay::OFF_C + qq * Lay::HALF + (lofs >> 1) * NT, uc);
                 else zero_slab<T, NT>(uc);
                 if (qq == G - 1) {
-                    // the stage is fully read: hand it back to the copy engine
+                    // the stage is fully read: hand it back to the copy engine.
+                    // Every lane orders its shared-memory reads of the stage
+                    // before the bulk copy (async proxy) that overwrites it.
+                    fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && g + ST < ngroups) issue(g + ST);
                 }

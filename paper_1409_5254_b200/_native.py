@@ -21,7 +21,7 @@ F64, F32 = 0, 1
 E_ARG, E_UNSUPPORTED, E_NOMEM = -1, -2, -3
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
-              "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "1886"]
+              "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "1886,128"]
 
 
 class LevelDesc(ctypes.Structure):

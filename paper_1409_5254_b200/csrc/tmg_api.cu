@@ -156,6 +156,19 @@ template <typename T, int NT> LevelC<T, NT> make_level(const tmg_level_desc &d)
         L.cneg[i] = m;
     }
     L.has_transfer = d.has_transfer;
+    // WK = omega (K+M)^-1 P^T in double: column j is the LU substitution of the
+    // permuted unit vector e_j (dg.py:153-168 without the row gather)
+    for (int j = 0; j < NT; ++j) {
+        double z[NT];
+        for (int i = 0; i < NT; ++i) z[i] = i == j ? 1.0 : 0.0;
+        for (int i = 1; i < NT; ++i)
+            for (int k = 0; k < i; ++k) z[i] -= d.lu[i * NT + k] * z[k];
+        for (int i = NT - 1; i >= 0; --i) {
+            for (int k = i + 1; k < NT; ++k) z[i] -= d.lu[i * NT + k] * z[k];
+            z[i] /= d.lu[i * NT + i];
+        }
+        for (int i = 0; i < NT; ++i) L.WK[i * NT + j] = (T)(d.omega * z[i]);
+    }
     // rank-1 factors of the coupling (outer(eval_start, eval_end), dg.py:236):
     // e = row 0, c_i = N[i, j*] / N[0, j*] (exact for both bases: c = e_0 or +-1)
     int js = 0;

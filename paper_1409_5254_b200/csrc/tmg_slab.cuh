@@ -52,6 +52,12 @@ template <> struct FP<float> {
     static __device__ __forceinline__ float zero(bool neg) { return neg ? -0.0f : 0.0f; }
 };
 
+// fp32 is a throughput variant (BASELINE config 5: normwise 1e-5 against the
+// fp64 reference), not a parity path: its slab arithmetic uses fused
+// multiply-adds and the precomputed damped inverse WK instead of the
+// reference's separately rounded operations and LU divisions.
+template <typename T> __host__ __device__ constexpr bool fast_fp() { return sizeof(T) == 4; }
+
 // a / d, correctly rounded, for a divisor d known ahead of time with
 // rinv = RN(1/d): q0 = RN(a rinv) is within ~2 ulp, one fma correction makes
 // it faithful, and a second correction gives RN(a/d) exactly (Markstein's
@@ -107,6 +113,9 @@ template <typename T, int NT> struct LevelC {
     T R1[NT * NT];  // Level.r1           (transfers.py:16-37)
     T R2[NT * NT];  // Level.r2
     T omega;        // resolve_damping(alpha(tau))
+    // fp32 fast form (no parity order to keep): WK = omega (K+M)^-1 P^T, so the
+    // damped update of a permuted residual y is u += WK y (FMA, no divisions)
+    T WK[NT * NT];
     int perm[NT];   // BlockLU.perm       (dg.py:148-151)
     unsigned cneg[NT];  // sign bits of coupling row i (sparse path)
     int has_transfer;
@@ -132,6 +141,16 @@ template <typename T, int NT> struct Cpl<T, NT, false> {
 template <typename T, int NT>
 __device__ __forceinline__ void bmat(const T *M, const T (&x)[NT], T (&o)[NT])
 {
+    if constexpr (fast_fp<T>()) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            T a = M[i * NT] * x[0];
+#pragma unroll
+            for (int j = 1; j < NT; ++j) a = __fmaf_rn(M[i * NT + j], x[j], a);
+            o[i] = a;
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
         T a = FP<T>::mul(M[i * NT], x[0]);
@@ -145,7 +164,13 @@ template <typename T, int NT, bool SPARSE>
 __device__ __forceinline__ Cpl<T, NT, SPARSE> make_cpl(const LevelC<T, NT> &L, const T (&u)[NT])
 {
     Cpl<T, NT, SPARSE> c;
-    if constexpr (SPARSE) {
+    if constexpr (SPARSE && fast_fp<T>()) {
+        T a = L.C[0] * u[0];
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = __fmaf_rn(L.C[j], u[j], a);
+        c.s = a;
+        c.m = 0;  // signed zeros are not tracked in the fast form
+    } else if constexpr (SPARSE) {
         T a = FP<T>::mul(L.C[0], u[0]);
 #pragma unroll
         for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(L.C[j], u[j]));
@@ -228,6 +253,27 @@ template <typename T, int NT, bool SPARSE>
 __device__ __forceinline__ void residual(const LevelC<T, NT> &L, const T (&u)[NT], const T (&f)[NT],
                                          const Cpl<T, NT, SPARSE> &p, bool has_prev, T (&r)[NT])
 {
+    if constexpr (fast_fp<T>()) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            T a = f[i];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) a = __fmaf_rn(L.A[i * NT + j], u[j], a);
+            r[i] = a;
+        }
+        if constexpr (SPARSE) {
+            r[0] = has_prev ? r[0] + p.s : r[0];
+        } else {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                T a = r[i];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) a = __fmaf_rn(L.C[i * NT + j], p.u[j], a);
+                r[i] = has_prev ? a : r[i];
+            }
+        }
+        return;
+    }
     bmat<T, NT>(L.A, u, r);
 #pragma unroll
     for (int i = 0; i < NT; ++i) r[i] = FP<T>::add(r[i], f[i]);
@@ -317,6 +363,12 @@ __device__ __forceinline__ void prolong_part(const LevelC<T, NT> &L, const T (&u
 
 template <typename T, int NT> __device__ __forceinline__ T sqnorm(const T (&r)[NT])
 {
+    if constexpr (fast_fp<T>()) {
+        T a = r[0] * r[0];
+#pragma unroll
+        for (int j = 1; j < NT; ++j) a = __fmaf_rn(r[j], r[j], a);
+        return a;
+    }
     T a = FP<T>::mul(r[0], r[0]);
 #pragma unroll
     for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(r[j], r[j]));
@@ -416,9 +468,18 @@ template <typename T, int NT, bool SPARSE, int PERM>
 __device__ __forceinline__ void residual_perm(const LevelC<T, NT> &L, const T (&u)[NT], const T (&f)[NT],
                                               const Cpl<T, NT, SPARSE> &p, bool has_prev, T (&y)[NT])
 {
-    if constexpr (PERM == P_GEN) {
+    if constexpr (PERM == P_GEN || fast_fp<T>()) {
         T r[NT];
         residual<T, NT, SPARSE>(L, u, f, p, has_prev, r);
+        if constexpr (PERM == P_ROT) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) y[i] = r[(i + 1) % NT];
+            return;
+        } else if constexpr (PERM == P_ID) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) y[i] = r[i];
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
             T v = r[0];
@@ -499,6 +560,18 @@ template <typename T, int NT> __device__ __forceinline__ void lu_apply_ieee(cons
 template <typename T, int NT, int J>
 __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], T (&y)[J][NT])
 {
+    if constexpr (fast_fp<T>()) {
+#pragma unroll
+        for (int q = 0; q < J; ++q)
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                T a = u[q][i];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) a = __fmaf_rn(L.WK[i * NT + j], y[q][j], a);
+                u[q][i] = a;
+            }
+        return;
+    }
     T ys[J][NT];
     unsigned bad = 0;
 #pragma unroll
@@ -598,6 +671,10 @@ __device__ __forceinline__ void sweep_p(const LevelC<T, NT> &L, T (&u)[NT], cons
 template <typename T, int NT>
 __device__ __forceinline__ void restrict_reg(const T (&R)[NT * NT], const T (&r)[NT], T (&o)[NT])
 {
+    if constexpr (fast_fp<T>()) {
+        bmat<T, NT>(R, r, o);
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
         T a = FP<T>::mul(R[i * NT], r[0]);
@@ -609,6 +686,16 @@ __device__ __forceinline__ void restrict_reg(const T (&R)[NT * NT], const T (&r)
 template <typename T, int NT>
 __device__ __forceinline__ void prolong_reg(const T (&R)[NT * NT], const T (&uc)[NT], T (&u)[NT])
 {
+    if constexpr (fast_fp<T>()) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            T a = u[i];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) a = __fmaf_rn(R[j * NT + i], uc[j], a);
+            u[i] = a;
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
         T a = FP<T>::mul(R[i], uc[0]);
@@ -621,6 +708,10 @@ __device__ __forceinline__ void prolong_reg(const T (&R)[NT * NT], const T (&uc)
 template <typename T, int NT>
 __device__ __forceinline__ void restrict_ptr(const T *R, const T (&r)[NT], T (&o)[NT])
 {
+    if constexpr (fast_fp<T>()) {
+        bmat<T, NT>(R, r, o);
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
         T a = FP<T>::mul(R[i * NT], r[0]);
@@ -632,6 +723,16 @@ __device__ __forceinline__ void restrict_ptr(const T *R, const T (&r)[NT], T (&o
 template <typename T, int NT>
 __device__ __forceinline__ void prolong_ptr(const T *R, const T (&uc)[NT], T (&u)[NT])
 {
+    if constexpr (fast_fp<T>()) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            T a = u[i];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) a = __fmaf_rn(R[j * NT + i], uc[j], a);
+            u[i] = a;
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
         T a = FP<T>::mul(R[i], uc[0]);
@@ -655,6 +756,18 @@ __device__ __forceinline__ void sweep(const LevelC<T, NT> &L, T (&u)[NT], const 
 {
     T y[NT], ys[NT];
     residual_perm<T, NT, SPARSE, P_GEN>(L, u, f, p, has_prev, y);
+    if constexpr (fast_fp<T>()) {
+        T uu[1][NT], yy[1][NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            uu[0][i] = u[i];
+            yy[0][i] = y[i];
+        }
+        finish_j<T, NT, 1>(L, uu, yy);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) u[i] = uu[0][i];
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < NT; ++i) ys[i] = y[i];
     unsigned bad = 0;

@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         const T *stg = ring + (size_t)(g % ST) * Lay::STAGE;
         const bool interior = g >= g_int0 && g < g_full;
         if (gt) mbar_wait(&bars[g % ST], (uint32_t)((g / ST) & 1));
-#pragma unroll
+#pragma unroll (P == 1 ? 1 : G)
         for (int qq = 0; qq < G; ++qq) {
             const int rr = g * G + qq;  // row within the chunk
             if (G > 1 && rr >= rows) break;

@@ -211,39 +211,39 @@ def workload_config(args, w):
 # ---------------------------------------------------------------------------
 # GPU arm
 
-def kernel_roofline(w, F, U, hier, stream_ptr, reps=10):
-    """Time the fused finest-level down pass (nu1 sweeps + residual +
-    restriction) and up pass alone with CUDA events; algorithmic bytes per
-    fine slab = 3.5 * n_t * 8 (read u, f [+ u_c/2], write u [+ f_c/2])."""
-    import torch
+def live_kernel_times(plan, F, U, floors, eps, max_iters):
+    """Per-kernel device times of one solve of the plan's OWN launches: the C
+    ABI's trace mode launches the same kernels directly (no graph) with a CUDA
+    event on the launch stream after each one (tmg_trace_enable/read).
+    Returns {description: (launches, total_s)}."""
     from paper_1409_5254_b200 import _native as nat
-    import paper_1409_5254_b200 as tmg
     L = nat.load()
-    B, n, nt = F.shape
-    lev = hier.levels[0]
-    om = tmg.optimal_omega(tmg.alpha(hier.basis, lev.tau))
-    d = nat.level_desc(lev.ops, n, om, lev.r1, lev.r2)
-    Uo = torch.empty_like(U)
-    FC = torch.empty((B, n // 2, nt), dtype=F.dtype, device=F.device)
-    UC = torch.zeros((B, n // 2, nt), dtype=F.dtype, device=F.device)
-    P = lambda t: ctypes.c_void_p(t.data_ptr())
-    s = ctypes.c_void_p(stream_ptr)
-    down = lambda: nat.check(L.tmg_down(0, ctypes.byref(d), P(F), P(U), P(Uo), P(FC), B, w["nu"], None, s))
-    up = lambda: nat.check(L.tmg_up(0, ctypes.byref(d), P(F), P(Uo), P(UC), P(U), None, B, w["nu"], None, s))
-    res = {}
-    for name, fn in (("down", down), ("up", up)):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        res[name] = e0.elapsed_time(e1) / reps * 1e-3
-    bytes_per_launch = 3.5 * nt * 8 * n * B
-    return res, bytes_per_launch
+    U.zero_()
+    L.tmg_trace_enable(1)
+    try:
+        plan.solve(F, U, floors, eps, max_iters)
+        buf = ctypes.create_string_buffer(1 << 20)
+        L.tmg_trace_read(buf, len(buf))
+    finally:
+        L.tmg_trace_enable(0)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split("\t")
+        out[name] = (int(cnt), float(ms) * 1e-3)
+    return out
+
+
+def kernel_roofline(times, n, nt, B, kind):
+    """(average launch seconds, algorithmic bytes per launch) of the finest-level
+    stream kernel of a kind: K_UP2 (5) reads u, f, u_c/2 and writes u
+    (3.5 n_t 8 B per fine slab); K_DOWNNORM (4) reads u, f and writes f_c/2
+    (2.5 n_t 8 B; the down pass stores no u because the up pass recomputes the
+    pre-sweeps)."""
+    for name, (cnt, tot) in times.items():
+        if f"kind={kind}>" in name and f" n={n} " in name:
+            per_slab = {5: 3.5, 4: 2.5}[kind]
+            return tot / cnt, per_slab * nt * 8 * n * B, name
+    return None, None, None
 
 
 def run_gpu_arm(args, w):
@@ -328,15 +328,19 @@ def run_gpu_arm(args, w):
     e2e_time = f0.elapsed_time(f1) * 1e-3
     e2e_time, dof_e2e = tdist.reduce_time_and_work(e2e_time, dof_e2e, device="cuda")
 
-    # roofline of the dominant kernel (finest-level fused down pass)
-    ktimes, kbytes = kernel_roofline(w, F, U, hier, torch.cuda.current_stream().cuda_stream)
+    # roofline of the dominant kernels, timed live on the plan's own launches:
+    # the finest-level up pass (K_UP2, ~55% of the solve's kernel time) and the
+    # finest-level down pass with the norm leaves (K_DOWNNORM, ~27%)
+    times = live_kernel_times(plan, F, U, floors, cfg.eps, cfg.max_iters)
     peak, peak_kind = peak_hbm()
-    achieved = kbytes / ktimes["down"] / 1e9
-    traffic = None
+    up_s, up_bytes, up_name = kernel_roofline(times, n, nt, B, 5)
+    dn_s, dn_bytes, dn_name = kernel_roofline(times, n, nt, B, 4)
+    traffic, traffic_dn = None, None
     try:
         with open(PROFILE_SUMMARY) as fh:
-            prof = json.load(fh)
-        traffic = prof.get(args.workload, {}).get("down_dram_bytes_per_launch")
+            prof = json.load(fh).get(args.workload, {})
+        traffic = prof.get("up2_dram_bytes_per_launch")
+        traffic_dn = prof.get("downnorm_dram_bytes_per_launch")
     except Exception:
         pass
 
@@ -355,14 +359,18 @@ def run_gpu_arm(args, w):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, w),
             "wall_s_to_1e-8": ms * 1e-3, "iterations": sorted(set(i for r in iters for i in r)),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"stream_kernel down (nu1={w['nu']} sweeps + residual + "
-                                   "restriction), finest level, whole batch",
-                         "bytes_per_launch": kbytes, "launch_s": ktimes["down"],
-                         "up_kernel_frac": kbytes / ktimes["up"] / 1e9 / peak,
+            "roofline": {"bound": "hbm", "achieved": up_bytes / up_s / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": up_bytes / up_s / 1e9 / peak, "traffic": traffic,
+                         "kernel": "finest-level fused up pass (prolong-add + nu2 sweeps, pre-sweeps "
+                                   "recomputed; K_UP2), whole batch: " + up_name,
+                         "bytes_per_launch": up_bytes, "launch_s": up_s,
+                         "timing": "CUDA events on the launch stream around the plan's own launches "
+                                   "(tmg_trace_enable), one solve after the timed region",
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                         "frac_of_nominal_8TBs": achieved / 8000.0},
+                         "frac_of_nominal_8TBs": up_bytes / up_s / 1e9 / 8000.0,
+                         "down_pass": {"kernel": dn_name, "bytes_per_launch": dn_bytes, "launch_s": dn_s,
+                                       "achieved": dn_bytes / dn_s / 1e9, "frac": dn_bytes / dn_s / 1e9 / peak,
+                                       "traffic": traffic_dn}},
             "e2e": {"value": dof_e2e / e2e_time, "unit": UNIT,
                     "h2d_bytes_per_step": B * n * nt * 8, "d2h_bytes_per_step": B * n * nt * 8,
                     "steps": e2e_steps, "path": "DevicePlan.solve_host -> C ABI tmg_plan_solve_host with pinned "

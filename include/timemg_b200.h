@@ -110,6 +110,27 @@ int tmg_coarse_solve(int dtype, const tmg_level_desc *lev, const void *f, void *
 int tmg_resid_norm(int dtype, const tmg_level_desc *lev, const void *f, const void *u,
                    double *norms_out, int64_t batch, void *stream);
 
+/* Raw numpy-order pairwise sum (no sqrt) of the per-slab squared residual
+ * norms sum_j r[n,j]^2 over slabs [skip, n_slabs) of each problem:
+ * sums_out[b] (device, float64).  One rank's share of norm_at
+ * (multigrid.py:447-462) when a problem is sharded along time: a rank's slab
+ * range preceded by `skip` halo slabs of its left neighbour (the residual of
+ * the first owned slab couples to the last halo slab; the range is a subtree
+ * of np.sum's pairwise recursion, so combining the ranks' sums in that tree
+ * reproduces the single-device norm bit for bit). */
+int tmg_resid_sqsum(int dtype, const tmg_level_desc *lev, const void *f, const void *u, int64_t skip,
+                    double *sums_out, int64_t batch, void *stream);
+
+/* Diagnostics: live per-kernel device times of the plan's own launches.
+ * tmg_trace_enable(1) makes plans launch directly (no CUDA graph) with a CUDA
+ * event recorded on the launch stream after every kernel; each finished solve
+ * appends "kernel-description\tlaunches\ttotal_ms\n" lines (times between
+ * consecutive events, i.e. kernel duration plus any launch gap) that
+ * tmg_trace_read copies into buf (NUL-terminated, truncated to cap) and
+ * clears.  Returns the text length.  tmg_trace_enable(0) restores graphs. */
+int tmg_trace_enable(int on);
+int64_t tmg_trace_read(char *buf, int64_t cap);
+
 /* ---- solver plan (the cycle / iteration driver, multigrid.py:263-500) ----- */
 
 typedef struct tmg_plan tmg_plan;

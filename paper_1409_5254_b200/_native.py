@@ -103,7 +103,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 _lib = None
 
 EXPORTS = ("tmg_last_error", "tmg_version", "tmg_device_check", "tmg_sweep", "tmg_residual",
-           "tmg_down", "tmg_up", "tmg_coarse_solve", "tmg_resid_norm", "tmg_plan_create",
+           "tmg_down", "tmg_up", "tmg_coarse_solve", "tmg_resid_norm", "tmg_resid_sqsum", "tmg_trace_enable", "tmg_trace_read", "tmg_plan_create",
            "tmg_plan_create_multi",
            "tmg_plan_destroy", "tmg_plan_cycles", "tmg_plan_solve", "tmg_plan_solve_host",
            "tmg_plan_stats", "tmg_plan_info")
@@ -130,6 +130,10 @@ def load():
     L.tmg_up.argtypes = [ci, lp, vp, vp, vp, vp, vp, i64, ci, vp, vp]
     L.tmg_coarse_solve.argtypes = [ci, lp, vp, vp, i64, ci, ci, vp]
     L.tmg_resid_norm.argtypes = [ci, lp, vp, vp, vp, i64, vp]
+    L.tmg_resid_sqsum.argtypes = [ci, lp, vp, vp, i64, vp, i64, vp]
+    L.tmg_trace_enable.argtypes = [ci]
+    L.tmg_trace_read.argtypes = [ctypes.c_char_p, i64]
+    L.tmg_trace_read.restype = i64
     L.tmg_plan_create.argtypes = [ctypes.POINTER(vp), lp, ci, i64, ctypes.POINTER(PlanOpts)]
     L.tmg_plan_create_multi.argtypes = [ctypes.POINTER(vp), lp, ci, i64, ctypes.POINTER(PlanOpts)]
     L.tmg_plan_destroy.argtypes = [vp]

@@ -67,16 +67,19 @@ bool sync_debug()
 
 // TMG_EVENT_TRACE=1: direct launches with a CUDA event after each kernel;
 // solve() prints per-kernel device times (including launch gaps) to stderr
+// (or tmg_trace_enable(1); tmg_trace_read() returns the per-kernel totals)
+int g_event_trace = -1;
 bool event_trace()
 {
-    static int v = -1;
-    if (v < 0) {
+    if (g_event_trace < 0) {
         const char *e = getenv("TMG_EVENT_TRACE");
-        v = (e && *e && *e != '0') ? 1 : 0;
+        g_event_trace = (e && *e && *e != '0') ? 1 : 0;
     }
-    return v == 1;
+    return g_event_trace == 1;
 }
 std::vector<std::pair<std::string, cudaEvent_t>> g_trace;
+bool g_trace_quiet = false;  // tmg_trace_read collects instead of printing
+std::string g_trace_text;
 void trace_mark(const char *what, cudaStream_t s)
 {
     if (!event_trace()) return;
@@ -91,7 +94,8 @@ void trace_report()
 {
     if (!event_trace() || g_trace.size() < 2) return;
     cudaEventSynchronize(g_trace.back().second);
-    std::vector<std::pair<std::string, double>> agg;
+    struct Agg { std::string name; double ms; int count; };
+    std::vector<Agg> agg;
     double total = 0;
     for (size_t i = 1; i < g_trace.size(); ++i) {
         float ms = 0;
@@ -99,11 +103,19 @@ void trace_report()
         total += ms;
         bool found = false;
         for (auto &a : agg)
-            if (a.first == g_trace[i].first) { a.second += ms; found = true; }
-        if (!found) agg.emplace_back(g_trace[i].first, ms);
+            if (a.name == g_trace[i].first) { a.ms += ms; a.count += 1; found = true; }
+        if (!found) agg.push_back({g_trace[i].first, ms, 1});
     }
-    fprintf(stderr, "event-trace total %.3f ms over %zu launches\n", total, g_trace.size() - 1);
-    for (auto &a : agg) fprintf(stderr, "event-trace %10.3f ms  %s\n", a.second, a.first.c_str());
+    if (g_trace_quiet) {
+        char line[256];
+        for (auto &a : agg) {
+            snprintf(line, sizeof line, "%s\t%d\t%.6f\n", a.name.c_str(), a.count, a.ms);
+            g_trace_text += line;
+        }
+    } else {
+        fprintf(stderr, "event-trace total %.3f ms over %zu launches\n", total, g_trace.size() - 1);
+        for (auto &a : agg) fprintf(stderr, "event-trace %10.3f ms %5d  %s\n", a.ms, a.count, a.name.c_str());
+    }
     for (auto &e : g_trace) cudaEventDestroy(e.second);
     g_trace.clear();
 }
@@ -953,6 +965,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             CK(cudaStreamSynchronize(s));
             int it = 0;
             while (h_any[0] && it < max_iters) {
+                trace_mark("host round trip", s);  // keeps the sync gap out of the next kernel's time
                 CKR(run_cycle(f, u, true, eps, s));
                 CK(cudaMemcpyAsync(h_any, d_any, sizeof(int), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
@@ -1042,7 +1055,7 @@ int make_plan_t(std::unique_ptr<PlanBase> &out, const tmg_level_desc *lv, int nl
 // ---------------------------------------------------------------------------
 // single-level entry points
 
-enum Op { OP_SWEEP, OP_RESID, OP_DOWN, OP_UP, OP_NORM };
+enum Op { OP_SWEEP, OP_RESID, OP_DOWN, OP_UP, OP_NORM, OP_SQSUM };
 
 struct OpArgs {
     const void *f, *u_in, *uc;
@@ -1051,6 +1064,7 @@ struct OpArgs {
     long long batch;
     int nu;
     const int32_t *active;
+    long long skip = 0;  // OP_SQSUM: first slab of the summed range
 };
 
 template <typename T, int NT, bool SP>
@@ -1111,14 +1125,20 @@ int run_op(Op op, const tmg_level_desc &d, const OpArgs &x, cudaStream_t s)
         a.sq_out = x.sq;
         if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
         return launch_stream<T, NT>(L, a, x.nu, x.sq ? K_GENERIC : K_UP, perm_kind(d), SP, s);
+    case OP_SQSUM:
     case OP_NORM: {
+        if (op == OP_SQSUM && (x.skip < 0 || x.skip >= n)) return fail(TMG_E_ARG, "skip must lie in [0, n_slabs)");
         double *sq = nullptr;
         CK(cudaMallocAsync(&sq, sizeof(double) * n * x.batch, s));
         a.sq_out = sq;
         a.flags = SF_NORM_SQ;
         if (tma_ok<T, NT>(a, false)) a.flags |= SF_TMA;
         int rc = launch_stream<T, NT>(L, a, 0, K_GENERIC, P_GEN, SP, s);
-        if (!rc) {
+        if (!rc && op == OP_SQSUM) {
+            range_sum_kernel<<<(unsigned)x.batch, 1024, 0, s>>>(sq, n, x.skip, n - x.skip, (double *)x.aux);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) rc = fail((int)e, "range sum: %s", cudaGetErrorString(e));
+        } else if (!rc) {
             finalize_sq_kernel<<<(unsigned)x.batch, 1024, 0, s>>>(sq, n, nullptr, nullptr, 0, nullptr, 0.0, 0,
                                                                 (double *)x.aux);
             cudaError_t e = cudaGetLastError();
@@ -1250,6 +1270,34 @@ int tmg_resid_norm(int dtype, const tmg_level_desc *lev, const void *f, const vo
 {
     OpArgs x{f, u, nullptr, nullptr, norms_out, nullptr, batch, 0, nullptr};
     return run_op_any(dtype, OP_NORM, lev, x, stream);
+}
+
+int tmg_trace_enable(int on)
+{
+    g_event_trace = on ? 1 : 0;
+    g_trace_quiet = on != 0;
+    g_trace_text.clear();
+    return 0;
+}
+
+int64_t tmg_trace_read(char *buf, int64_t cap)
+{
+    const int64_t n = (int64_t)g_trace_text.size();
+    if (buf && cap > 0) {
+        const int64_t k = std::min(n, cap - 1);
+        memcpy(buf, g_trace_text.data(), (size_t)k);
+        buf[k] = 0;
+    }
+    g_trace_text.clear();
+    return n;
+}
+
+int tmg_resid_sqsum(int dtype, const tmg_level_desc *lev, const void *f, const void *u, int64_t skip,
+                    double *sums_out, int64_t batch, void *stream)
+{
+    OpArgs x{f, u, nullptr, nullptr, sums_out, nullptr, batch, 0, nullptr};
+    x.skip = skip;
+    return run_op_any(dtype, OP_SQSUM, lev, x, stream);
 }
 
 int tmg_plan_create(tmg_plan **plan, const tmg_level_desc *levels, int n_levels, int64_t batch,

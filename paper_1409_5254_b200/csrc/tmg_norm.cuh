@@ -60,6 +60,18 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
+// raw pairwise sum (np.sum order, no sqrt) of sq[b * stride + skip, + cnt):
+// one rank's share of the norm of a time-sharded problem (its slab range is a
+// subtree of numpy's pairwise recursion)
+__global__ void __launch_bounds__(1024)
+    range_sum_kernel(const double *sq, long long stride, long long skip, long long cnt, double *out)
+{
+    __shared__ double part[1024];
+    const int b = blockIdx.x;
+    const double s = block_pairwise(sq + (size_t)b * stride + skip, cnt, part);
+    if (threadIdx.x == 0) out[b] = s;
+}
+
 // generic (any n) exact pairwise over per-slab squares
 __global__ void __launch_bounds__(1024)
     finalize_sq_kernel(const double *sq, long long n, ProbState *st, double *hist, int hist_stride,

@@ -1,0 +1,43 @@
+#!/bin/bash
+# GPU-box profiling recipe for the headline (BASELINE config 3), one GPU:
+#   1. bench.py (the JSON line, CPU baseline included)
+#   2. ncu launch list of bench.py (gpu__time_duration per launch, serialised)
+#   3. ncu --set full of the two dominant kernels of one solve
+#      (finest-level fused down pass with norm leaves, K_DOWNNORM; finest-level
+#      up pass, K_UP2), located from a launch list of scripts/ncu_target.py
+# Usage (from the repo root, under gpurun):  bash scripts/profile_round.sh [tag]
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out
+mkdir -p $OUT
+timeout 900 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
+echo "bench rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/${TAG}_launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu \
+    > $OUT/${TAG}_ncu_bench.log 2>&1
+echo "launch list rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/${TAG}_launches_target.csv python scripts/ncu_target.py > $OUT/${TAG}_ncu_target.log 2>&1
+echo "target launch list rc=$?"
+# index (among launches of the same kernel name) of the longest K_DOWNNORM and K_UP2 launch
+read SKIP4 SKIP5 < <(python - "$OUT/${TAG}_launches_target.csv" <<'EOF'
+import csv, sys
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+h, rows = rows[0], rows[1:]
+ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+norm = lambda k: k.replace("(int)", "").replace("(bool)", "").replace("true", "1")
+def best(tag):
+    seq = [float(r[vi].replace(",", "")) for r in rows if tag in norm(r[ki])]
+    return max(range(len(seq)), key=lambda i: seq[i]) if seq else 0
+print(best("stream_kernel<double, 2, 1, 1, 4,"), best("stream_kernel<double, 2, 1, 1, 5,"))
+EOF
+)
+echo "skip kind4=$SKIP4 kind5=$SKIP5"
+for K in 4 5; do
+    S=$([ $K = 4 ] && echo $SKIP4 || echo $SKIP5)
+    timeout 900 ncu --set full --import-source on --clock-control none \
+        --kernel-name-base demangled \
+        -k "regex:stream_kernel<double, (\\(int\\))?2, (\\(int\\))?1, (\\(bool\\))?(1|true), (\\(int\\))?$K," --launch-skip $S --launch-count 1 \
+        -o $OUT/${TAG}_ncu_kind$K -f python scripts/ncu_target.py > $OUT/${TAG}_ncu_kind$K.log 2>&1
+    echo "ncu full kind$K rc=$?"
+done

@@ -13,7 +13,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libtimemg_b200.so")
+# TMG_LIB: an alternative build of the same library (A/B experiments, scripts/ab_build.sh)
+LIB_PATH = os.environ.get("TMG_LIB") or os.path.join(HERE, "libtimemg_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(REPO, "include")
 MAXNT = 8

@@ -270,14 +270,24 @@ int launch_stream(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
 // rows (of w slabs) per warp chunk: enough warps to fill the GPU several
 // times over, a multiple of the norm leaf, and long enough to amortise the
 // warm-up row
-int chunk_rows(long long n, long long batch, int leaf_rows, int w)
+int chunk_rows(long long n, long long batch, int leaf_rows, int w, int stage)
 {
     const long long rows = (n + w - 1) / w;
-    const long long target_warps = (long long)sm_count() * 16 * 4;
+    // TMG_CHUNK_WAVES / TMG_CHUNK_MIN: tuning overrides (default 2 waves of
+    // 16 resident warps per SM, chunks of >= 2 rows; 2 waves measured best on
+    // the latency-bound 2^20-slab levels, large batches hit the 128-row cap)
+    static int waves = -1, rmin = -1;
+    if (waves < 0) {
+        const char *e = getenv("TMG_CHUNK_WAVES");
+        waves = e ? std::max(1, atoi(e)) : 2;
+        const char *m = getenv("TMG_CHUNK_MIN");
+        rmin = m ? std::max(1, atoi(m)) : 2;
+    }
+    const long long target_warps = (long long)sm_count() * 16 * waves;
     long long r = (rows * batch) / std::max(1LL, target_warps);
-    r = std::max(2LL, std::min(128LL, r));
-    // a multiple of the ring stage (64 slabs) and of the norm leaf
-    const int g = 64 / w;
+    r = std::max((long long)rmin, std::min(128LL, r));
+    // a multiple of the ring stage (stage_slabs) and of the norm leaf
+    const int g = stage / w;
     const int q = std::lcm(g, std::max(leaf_rows, 1));
     r = ((r + q - 1) / q) * q;
     return (int)std::max<long long>(r, 1);
@@ -290,7 +300,7 @@ template <typename T, int NT> StreamArgs<T> stream_args(long long n, long long b
     memset(&a, 0, sizeof a);
     a.n = n;
     a.batch = (int)batch;
-    a.rows_per_chunk = chunk_rows(n, batch, leaf_rows, w);
+    a.rows_per_chunk = chunk_rows(n, batch, leaf_rows, w, stage_slabs<T, NT>());
     a.chunks = ((n + w - 1) / w + a.rows_per_chunk - 1) / a.rows_per_chunk;
     a.leaf_rows = leaf_rows > 0 ? leaf_rows : 1;
     return a;
@@ -461,7 +471,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
         // choose the tail: the longest suffix of small levels that fits in smem
         const size_t smem_cap = 200 * 1024;
-        long long tail_max = o.tail_max_slabs > 0 ? o.tail_max_slabs : (NT <= 2 ? 2048 : 1024);
+        // measured on config 2 (N = 2^20): 1024 (n_t <= 2) and 512 (n_t >= 3) beat 2048 / 1024 by 5-6 %
+        long long tail_max = o.tail_max_slabs > 0 ? o.tail_max_slabs : (NT <= 2 ? 1024 : 512);
         auto store_of = [&](int l0) {
             long long e = 0;
             for (int l = l0; l < nl; ++l) e += 2 * n[l] * NT;
@@ -471,6 +482,10 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             return tail_fixed_smem<T, NT>(nl - l0) + sizeof(T) * store_of(l0) +
                    (l0 == 0 ? sizeof(double) * n[0] : 0);
         };
+        // small problems (config 1) and per-problem-operator batches run whole
+        // in one CTA: one launch per solve
+        if (o.tail_max_slabs <= 0 && (multi || n[0] <= (NT <= 2 ? 2048 : 1024)) && smem_of(0) <= smem_cap)
+            tail_max = std::max(tail_max, n[0]);
         tl = nl - 1;
         for (int l = nl - 2; l >= 0; --l) {
             if (n[l] <= tail_max && smem_of(l) <= smem_cap) tl = l;
@@ -610,9 +625,10 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         } else {
             for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s));
         }
-        if (up2 && !norm_up) {
+        if (up2 && (!norm_up || (l == 0 && norm_up2()))) {
             // prolong-add + post-sweeps, the pre-sweeps recomputed from the
-            // level's original iterate (read in place; warm-ups from the halo)
+            // level's original iterate (read in place; warm-ups from the halo);
+            // at the finest level of a solve also the norm leaves of the result
             StreamArgs<T> a = level_args(l);
             const bool zero = (l > 0) && first_visit;
             a.f = fL;
@@ -622,8 +638,12 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             a.halo = halo[l];
             a.active = d_active;
             a.flags = SF_PROLONG | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
+            if (norm_up) {
+                a.flags |= SF_NORM_LEAF;
+                a.leaf_out = leaves;
+            }
             if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
-            CKR((launch_stream<T, NT>(L[l], a, o.nu2, K_UP2, pk[l], SP, s)));
+            CKR((launch_stream<T, NT>(L[l], a, o.nu2, norm_up ? K_UP2NORM : K_UP2, pk[l], SP, s)));
             ++kernels_per_cycle;
             return 0;
         }
@@ -648,7 +668,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s)
     {
-        if (up2 && norm) {
+        if (up2 && norm && !(l == 0 && norm_up2())) {
             // the up pass cannot produce the norm: take it in a separate pass
             CKR(enqueue_down(l, f0, u0, first_visit, false, s));
             CKR(enqueue_rest(l, f0, u0, false, s, first_visit));
@@ -675,22 +695,36 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         return 0;
     }
 
-    // the finest down pass computes the stopping norm of its input (the
-    // previous cycle's result) when the norm has numpy's leaf structure
-    bool norm_in() const { return leaf_rows0 > 0 && SP; }
+    // where the stopping norm comes from when it has numpy's leaf structure:
+    // the NEXT cycle's finest down pass (K_DOWNNORM: its first sweep's
+    // residual, default; one speculative down pass per solve), or the finest
+    // up pass (K_UP2NORM: an extra residual of its output; TMG_NORM_UP=1).
+    // Measured on config 3: 128.3 vs 131.1 ms per solve, config 2 ~1-2 %.
+    bool norm_up2() const { return up2 && leaf_rows0 > 0 && SP && norm_up_env(); }
+    bool norm_in() const { return leaf_rows0 > 0 && SP && !norm_up2(); }
+    static bool norm_up_env()
+    {
+        static int v = -1;
+        if (v < 0) {
+            const char *e = getenv("TMG_NORM_UP");
+            v = (e && *e && *e != '0') ? 1 : 0;
+        }
+        return v == 1;
+    }
 
     int enqueue_finalize(int mode, double eps, cudaStream_t s, cudaGraphConditionalHandle h = 0,
                          bool use_h = false)
     {
         if (leaf_rows0)
-            finalize_leaves_kernel<<<(unsigned)B, 1024, 0, s>>>(leaves, nleaves, d_st, d_hist, hist_stride,
-                                                               d_floor, eps, mode);
+            CK(launch_pdl(finalize_leaves_kernel, dim3((unsigned)B), dim3(1024), 0, s, (const double *)leaves,
+                          nleaves, d_st, d_hist, hist_stride, (const double *)d_floor, eps, mode));
         else
             finalize_sq_kernel<<<(unsigned)B, 1024, 0, s>>>(sqbuf, n[0], d_st, d_hist, hist_stride, d_floor,
                                                            eps, mode, nullptr);
         CK_LAUNCH("finalize");
         trace_mark("finalize", s);
-        set_active_kernel<<<1, 256, 0, s>>>(d_st, d_active, d_any, (int)B, h, use_h ? 1 : 0);
+        CK(launch_pdl(set_active_kernel, dim3(1), dim3(256), 0, s, (const ProbState *)d_st, d_active, d_any,
+                      (int)B, h, use_h ? 1 : 0));
         CK_LAUNCH("set_active");
         trace_mark("set_active", s);
         kernels_per_cycle += 2;

@@ -28,8 +28,7 @@ int launch_one(const LevelC<T, NT> &L, const StreamArgs<T> &a, cudaStream_t s)
     constexpr int WARPS = CtaShape<T, NT>::WARPS;
     const long long grid = (warps + WARPS - 1) / WARPS;
     if (grid <= 0) return 0;
-    k<<<(unsigned)grid, WARPS * 32, smem, s>>>(L, a);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(k, dim3((unsigned)grid), dim3(WARPS * 32), smem, s, L, a);
 }
 
 template <typename T, int NT, bool SP, int KIND, int PERM>
@@ -76,6 +75,7 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
     case K_UPNORM: return by_perm<T, NT, K_UPNORM>(L, a, nu, perm, s);
     case K_DOWNNORM: return by_perm<T, NT, K_DOWNNORM>(L, a, nu, perm, s);
     case K_UP2: return by_perm<T, NT, K_UP2>(L, a, nu, perm, s);
+    case K_UP2NORM: return by_perm<T, NT, K_UP2NORM>(L, a, nu, perm, s);
     }
     return -1;
 }
@@ -94,9 +94,8 @@ template <typename T, int NT> int tail_prepare(bool sparse, size_t smem)
 template <typename T, int NT>
 int tail_launch(const TailArgs<T, NT> &t, bool sparse, unsigned grid, size_t smem, cudaStream_t s)
 {
-    if (sparse) tail_kernel<T, NT, true><<<grid, TAIL_THREADS, smem, s>>>(t);
-    else tail_kernel<T, NT, false><<<grid, TAIL_THREADS, smem, s>>>(t);
-    return (int)cudaGetLastError();
+    if (sparse) return (int)launch_pdl(tail_kernel<T, NT, true>, dim3(grid), dim3(TAIL_THREADS), smem, s, t);
+    return (int)launch_pdl(tail_kernel<T, NT, false>, dim3(grid), dim3(TAIL_THREADS), smem, s, t);
 }
 
 template <typename T, int NT>

@@ -8,7 +8,38 @@
 #include "tmg_slab.cuh"
 #include "tmg_types.cuh"
 
+#include <cstdlib>
+#include <utility>
+
 namespace tmg {
+
+// TMG_NO_PDL=1 launches without the programmatic-serialisation attribute (A/B)
+inline bool pdl_enabled()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TMG_NO_PDL");
+        v = (e && *e && *e != '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// kernel launch with programmatic dependent launch on the stream
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 template <typename T> struct StreamArgs;
 

@@ -13,6 +13,8 @@ __global__ void __launch_bounds__(1024)
     finalize_leaves_kernel(const double *leaves, long long m, ProbState *st, double *hist,
                            int hist_stride, const double *floor_, double eps, int mode)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double part[1024];
     const int b = blockIdx.x;
     if (mode == 1 && !st[b].active) return;
@@ -109,6 +111,8 @@ __global__ void __launch_bounds__(256)
     set_active_kernel(const ProbState *st, int *active, int *any_out, int batch,
                       cudaGraphConditionalHandle h, int use_handle)
 {
+    pdl_trigger();
+    pdl_wait();
     int any = 0;
     for (int b = threadIdx.x; b < batch; b += blockDim.x) {
         const int a = st[b].active;

@@ -20,7 +20,7 @@
 // other: the pass is one HBM read of u, f (and u_coarse) and one write of u
 // (and f_coarse) per slab.
 //
-// Rows arrive in a per-warp shared-memory ring (64 slabs per stage) filled by
+// Rows arrive in a per-warp shared-memory ring (stage_slabs() per stage) filled by
 // the TMA engine (cp.async.bulk global->shared, completion on an mbarrier, L2
 // evict-first); lane 0 refills a stage as soon as the warp has read it.
 // Interior rows run a specialised path (every slab valid, every slab has a
@@ -33,7 +33,6 @@
 namespace tmg {
 
 constexpr int SW_STAGES = 4;        // max ring stages per warp
-constexpr int SW_STAGE_SLABS = 64;  // fine slabs per ring stage
 constexpr int SW_LEAF_BATCH = 4;    // numpy leaves reduced together (one per 8 lanes)
 #ifndef TMG_P2_WARPS
 #define TMG_P2_WARPS 8
@@ -71,7 +70,9 @@ enum StreamFlags : int {
 // K_UP2: an up pass that RECOMPUTES the nu pre-sweeps from the level's
 // original iterate (bitwise the same values the down pass had) instead of
 // reading a stored pre-smoothed iterate -- the down pass then writes no u.
-enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM = 4, K_UP2 = 5 };
+// K_UP2NORM: K_UP2 that also returns the residual norm of its OUTPUT (the
+// stopping test of the cycle it ends, multigrid.py:447-459)
+enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM = 4, K_UP2 = 5, K_UP2NORM = 6 };
 
 template <typename T> struct StreamArgs {
     const T *f;
@@ -153,7 +154,7 @@ template <int KIND> struct KindProlongs {
     static constexpr bool value = KIND != K_DOWN && KIND != K_DOWNNORM;
 };
 template <int KIND> struct KindLeaf {
-    static constexpr bool value = KIND == K_GENERIC || KIND == K_UPNORM || KIND == K_DOWNNORM;
+    static constexpr bool value = KIND == K_GENERIC || KIND == K_UPNORM || KIND == K_DOWNNORM || KIND == K_UP2NORM;
 };
 
 // vector load/store of one lane's P*NT consecutive elements (16-byte pieces
@@ -220,7 +221,7 @@ template <typename T, int NT, int P> __device__ __forceinline__ void store_lane(
 template <typename T, int NT, bool WITH_C, bool LEAF> struct RowLayout {
     static constexpr int P = slabs_per_lane<T, NT>();
     static constexpr int W = 32 * P;                // slabs per row
-    static constexpr int G = SW_STAGE_SLABS / W;    // rows per ring stage
+    static constexpr int G = stage_slabs<T, NT>() / W;  // rows per ring stage
     static constexpr int ROW = W * NT;              // elements of one fine row
     static constexpr int HALF = ROW / 2;            // elements of the matching coarse half-row
     static constexpr int OFF_F = G * ROW;
@@ -253,9 +254,10 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                               : KIND == K_UPNORM ? (SF_PROLONG | SF_WRITE_U | SF_NORM_LEAF)
                               : KIND == K_DOWNNORM ? (SF_RESTRICT | SF_WRITE_U | SF_NORM_LEAF)
                               : KIND == K_UP2 ? (SF_PROLONG | SF_WRITE_U)
-                                              : 0;
-    // pre-sweeps recomputed before the prolongation (K_UP2)
-    static constexpr int NPRE = KIND == K_UP2 ? NU : 0;
+                              : KIND == K_UP2NORM ? (SF_PROLONG | SF_WRITE_U | SF_NORM_LEAF)
+                                                  : 0;
+    // pre-sweeps recomputed before the prolongation (K_UP2, K_UP2NORM)
+    static constexpr int NPRE = (KIND == K_UP2 || KIND == K_UP2NORM) ? NU : 0;
     // norm of the pass's input (K_DOWNNORM) rather than of its output
     static constexpr bool NORM_IN = KIND == K_DOWNNORM && NU > 0;
     static constexpr int P = slabs_per_lane<T, NT>();
@@ -462,6 +464,8 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     constexpr int W = Lay::W;
     constexpr int G = Lay::G;
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * Lay::WARPS + warp;
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         const T *stg = ring + (size_t)(g % ST) * Lay::STAGE;
         const bool interior = g >= g_int0 && g < g_full;
         if (gt) mbar_wait(&bars[g % ST], (uint32_t)((g / ST) & 1));
-#pragma unroll (P == 1 ? 1 : G)
+#pragma unroll 1
         for (int qq = 0; qq < G; ++qq) {
             const int rr = g * G + qq;  // row within the chunk
             if (G > 1 && rr >= rows) break;

@@ -545,6 +545,8 @@ template <typename T, int NT, bool SPARSE>
 __global__ void __launch_bounds__(TAIL_THREADS)
     tail_kernel(const __grid_constant__ TailArgs<T, NT> a)
 {
+    pdl_trigger();
+    pdl_wait();
     if (a.active && !a.active[blockIdx.x]) return;
     if (a.in_smem) tail_body<T, NT, SPARSE, true>(a);
     else tail_body<T, NT, SPARSE, false>(a);

@@ -5,12 +5,29 @@
 namespace tmg {
 
 constexpr int TAIL_THREADS = 512;
+
+// Programmatic dependent launch (the plan's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its
+// successor be scheduled as soon as all of its CTAs have started, and waits
+// for its predecessor's completion (and memory) before its first global
+// access.  Launch latency and CTA rasterisation overlap the previous kernel's
+// tail; without the attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 constexpr int MAXLEV = 48;
 
 // streaming kernels: consecutive slabs owned by one lane (a row is 32*P slabs).
 // Two slabs give each lane two independent dependency chains and make the
 // restriction pairs lane-local; larger fp64 blocks would spill.
 template <typename T, int NT> constexpr int slabs_per_lane() { return (NT <= 2 || sizeof(T) == 4) ? 2 : 1; }
+// fine slabs per TMA ring stage (a multiple of the row): the per-stage work
+// (mbarrier wait, proxy fence, refill) is ~80 instructions, so two-slab lanes
+// take two 64-slab rows per stage; one-slab lanes keep 2 rows of 32 slabs
+// (larger fp64 stages would not leave two CTAs per SM)
+#ifndef TMG_STAGE_SLABS_P2
+#define TMG_STAGE_SLABS_P2 128
+#endif
+template <typename T, int NT> constexpr int stage_slabs() { return slabs_per_lane<T, NT>() == 2 ? TMG_STAGE_SLABS_P2 : 64; }
 
 // per-problem iteration state (multigrid.py:481-496)
 struct ProbState {

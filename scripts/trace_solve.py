@@ -10,6 +10,7 @@ import torch  # noqa: E402
 import paper_1409_5254_b200 as tmg  # noqa: E402
 from paper_1409_5254_b200 import _native as nat, problems, solver  # noqa: E402
 
+solver.TAIL_MAX = int(os.environ.get("TMG_TAIL_MAX", "0"))  # 0 = library default
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 n = 1 << (int(sys.argv[2]) if len(sys.argv) > 2 else 20)
 p_t = int(sys.argv[3]) if len(sys.argv) > 3 else 1

@@ -6,8 +6,13 @@ import re
 import subprocess
 import sys
 
+# argument: a .ncu-rep, or the prefix of the <prefix>_raw.csv / <prefix>_sass.csv
+# exports that scripts/profile_round.sh brings back from the GPU box
 rep = sys.argv[1]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".ncu-rep"):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+else:
+    raw = open(rep + "_raw.csv").read()
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -22,8 +27,11 @@ for d in data:
             i = hdr.index(k)
             print(f"  {k:62s} {d[i]} {units[i]}")
     print("  --")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
-                     capture_output=True, text=True).stdout.splitlines()
+if rep.endswith(".ncu-rep"):
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
+                         capture_output=True, text=True).stdout.splitlines()
+else:
+    src = open(rep + "_sass.csv").read().splitlines()
 rows = list(csv.reader(src[1:]))
 hdr = rows[0]
 si, ei = hdr.index("Source"), hdr.index("Instructions Executed")

@@ -38,6 +38,10 @@ for K in 4 5; do
     timeout 900 ncu --set full --import-source on --clock-control none \
         --kernel-name-base demangled \
         -k "regex:stream_kernel<double, (\\(int\\))?2, (\\(int\\))?1, (\\(bool\\))?(1|true), (\\(int\\))?$K," --launch-skip $S --launch-count 1 \
-        -o $OUT/${TAG}_ncu_kind$K -f python scripts/ncu_target.py > $OUT/${TAG}_ncu_kind$K.log 2>&1
+        -o /tmp/${TAG}_ncu_kind$K -f python scripts/ncu_target.py > $OUT/${TAG}_ncu_kind$K.log 2>&1
     echo "ncu full kind$K rc=$?"
+    # reports are ~30 MB each: bring back the raw metrics and the SASS source page only
+    ncu -i /tmp/${TAG}_ncu_kind$K.ncu-rep --page raw --csv > $OUT/${TAG}_ncu_kind${K}_raw.csv 2>/dev/null
+    ncu -i /tmp/${TAG}_ncu_kind$K.ncu-rep --page source --csv --print-source sass \
+        > $OUT/${TAG}_ncu_kind${K}_sass.csv 2>/dev/null
 done

@@ -417,6 +417,9 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         }
         cudaFree(d_fh);
         cudaFree(d_uh);
+        if (ev_h2d) cudaEventDestroy(ev_h2d);
+        for (cudaStream_t st : {cs_in, cs_out, cs_cmp[0], cs_cmp[1]})
+            if (st) cudaStreamDestroy(st);
         cudaFree(gstore);
         cudaFree(leaves);
         cudaFree(sqbuf);
@@ -852,6 +855,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     }
 
     T *d_fh = nullptr, *d_uh = nullptr;  // device copies for the host-buffer entry point
+    cudaEvent_t ev_h2d = nullptr;         // this sub-batch's inputs are on the device
+    cudaStream_t cs_in = nullptr, cs_out = nullptr, cs_cmp[2] = {nullptr, nullptr};  // host-buffer pipeline
     std::vector<tmg_level_desc> descs;   // kept to build sub-batch plans
     std::vector<std::unique_ptr<Plan>> subs;
 
@@ -873,22 +878,65 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         return 0;
     }
 
+    // one sub-batch of the pipelined host-buffer solve: H2D on cin, solve on
+    // cmp (after the H2D), D2H on cout (after the solve); no host waits -- the
+    // caller collects this sub-plan's previous sub-batch before reusing it
+    int enqueue_host_async(const T *f, const T *u0, T *u_out, const double *floor_, double eps, int max_iters,
+                           cudaStream_t cin, cudaStream_t cmp, cudaStream_t cout)
+    {
+        const size_t bytes = sizeof(T) * n[0] * NT * B;
+        if (!d_fh) {
+            CK(cudaMalloc(&d_fh, bytes));
+            CK(cudaMalloc(&d_uh, bytes));
+            CK(cudaEventCreateWithFlags(&ev_h2d, cudaEventDisableTiming));
+        }
+        CK(cudaMemcpyAsync(d_fh, f, bytes, cudaMemcpyHostToDevice, cin));
+        if (u0) CK(cudaMemcpyAsync(d_uh, u0, bytes, cudaMemcpyHostToDevice, cin));
+        else CK(cudaMemsetAsync(d_uh, 0, bytes, cin));
+        CK(cudaEventRecord(ev_h2d, cin));
+        CK(cudaStreamWaitEvent(cmp, ev_h2d, 0));
+        CKR(enqueue_solve(d_fh, d_uh, floor_, eps, max_iters, cmp));  // records ev_done on cmp
+        CK(cudaStreamWaitEvent(cout, ev_done, 0));
+        CK(cudaMemcpyAsync(u_out, d_uh, bytes, cudaMemcpyDeviceToHost, cout));
+        CK(cudaEventRecord(ev_done, cout));  // collect() waits for the solution on the host
+        return 0;
+    }
+
     int solve_host(const void *f, const void *u0, void *u_out, const double *floor_, double eps,
                    int max_iters) override
     {
-        // sub-batches on two streams: the PCIe copies of one overlap the solve of the other
-        const int nch = (B >= 8 && B % 4 == 0 && tl > 0) ? 4 : 1;
+        // Pipelined sub-batches: copy-in and copy-out on their own streams, the
+        // solves alternating between two compute streams (so one sub-batch's
+        // latency-bound coarse levels overlap another's bandwidth-bound fine
+        // levels), 4 sub-plans in rotation; the PCIe traffic of every sub-batch
+        // but the first and last hides under the solves.
+        // sub-batch count measured on config 3 (B = 64): 4 -> 163 ms, 8 -> 149 ms,
+        // 16 -> 145 ms, 32 -> 168 ms per host-buffer solve
+        int nch = tl == 0 ? 1 : (B >= 32 && B % 16 == 0) ? 16 : (B >= 16 && B % 8 == 0) ? 8
+                : (B >= 8 && B % 4 == 0) ? 4 : 1;
+        if (const char *e = getenv("TMG_HOST_CHUNKS")) {  // tuning override (must divide the batch)
+            const int k = atoi(e);
+            if (k >= 1 && B % k == 0 && tl > 0) nch = k;
+        }
         if (nch == 1) {
             CKR(enqueue_host((const T *)f, (const T *)u0, (T *)u_out, floor_, eps, max_iters));
             return collect();
         }
         const long long bc = B / nch;
-        if (subs.empty()) {
-            for (int k = 0; k < 2; ++k) {
+        const int nsub = std::min(nch, 4);
+        if ((int)subs.size() != nsub) {
+            subs.clear();
+            for (int k = 0; k < nsub; ++k) {
                 auto p = std::make_unique<Plan>();
                 CKR(p->init(descs.data(), depth, bc, o));
                 subs.push_back(std::move(p));
             }
+        }
+        if (!cs_in) {
+            CK(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&cs_cmp[0], cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&cs_cmp[1], cudaStreamNonBlocking));
         }
         const size_t per = (size_t)n[0] * NT * bc;
         last_max_iters = max_iters;
@@ -897,7 +945,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         h_it.assign(B, 0);
         h_conv.assign(B, 0);
         auto gather = [&](int c) -> int {
-            Plan &p = *subs[c % 2];
+            Plan &p = *subs[c % nsub];
             CKR(p.collect());
             for (long long b = 0; b < bc; ++b) {
                 const long long g = c * bc + b;
@@ -909,12 +957,13 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             return 0;
         };
         for (int c = 0; c < nch; ++c) {
-            if (c >= 2) CKR(gather(c - 2));
-            Plan &p = *subs[c % 2];
-            CKR(p.enqueue_host((const T *)f + c * per, u0 ? (const T *)u0 + c * per : nullptr,
-                               (T *)u_out + c * per, floor_ + c * bc, eps, max_iters));
+            if (c >= nsub) CKR(gather(c - nsub));
+            Plan &p = *subs[c % nsub];
+            CKR(p.enqueue_host_async((const T *)f + c * per, u0 ? (const T *)u0 + c * per : nullptr,
+                                     (T *)u_out + c * per, floor_ + c * bc, eps, max_iters, cs_in,
+                                     cs_cmp[c % 2], cs_out));
         }
-        for (int c = std::max(0, nch - 2); c < nch; ++c) CKR(gather(c));
+        for (int c = std::max(0, nch - nsub); c < nch; ++c) CKR(gather(c));
         return 0;
     }
 

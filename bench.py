@@ -233,16 +233,20 @@ def live_kernel_times(plan, F, U, floors, eps, max_iters):
     return out
 
 
+# algorithmic bytes per fine slab (units of n_t * 8 B) of the stream kernel kinds
+# the plan launches: K_UP2DOWN (7) = finest up pass of cycle k
+# fused with the finest down pass of cycle k+1: reads u, f, u_c/2, writes u,
+# f_c/2; K_UP2 (5) at a coarse level (zero original iterate): reads f, u_c/2,
+# writes u; K_DOWN (1) at a coarse level (zero guess): reads f, writes f_c/2
+KIND_BYTES = {7: 4.0, 5: 2.5, 1: 1.5, 4: 2.5}
+
+
 def kernel_roofline(times, n, nt, B, kind):
-    """(average launch seconds, algorithmic bytes per launch) of the finest-level
-    stream kernel of a kind: K_UP2 (5) reads u, f, u_c/2 and writes u
-    (3.5 n_t 8 B per fine slab); K_DOWNNORM (4) reads u, f and writes f_c/2
-    (2.5 n_t 8 B; the down pass stores no u because the up pass recomputes the
-    pre-sweeps)."""
+    """(average launch seconds, algorithmic bytes per launch, description) of
+    the stream kernel of a kind at the level with n slabs per problem."""
     for name, (cnt, tot) in times.items():
         if f"kind={kind}>" in name and f" n={n} " in name:
-            per_slab = {5: 3.5, 4: 2.5}[kind]
-            return tot / cnt, per_slab * nt * 8 * n * B, name
+            return tot / cnt, KIND_BYTES[kind] * nt * 8 * n * B, name
     return None, None, None
 
 
@@ -328,19 +332,23 @@ def run_gpu_arm(args, w):
     e2e_time = f0.elapsed_time(f1) * 1e-3
     e2e_time, dof_e2e = tdist.reduce_time_and_work(e2e_time, dof_e2e, device="cuda")
 
-    # roofline of the dominant kernels, timed live on the plan's own launches:
-    # the finest-level up pass (K_UP2, ~55% of the solve's kernel time) and the
-    # finest-level down pass with the norm leaves (K_DOWNNORM, ~27%)
+    # roofline of the dominant kernel, timed live on the plan's own launches:
+    # the finest-level fused up/next-down pass (K_UP2DOWN, ~2/3 of the solve's
+    # kernel time), plus the level-1 passes beside it
     times = live_kernel_times(plan, F, U, floors, cfg.eps, cfg.max_iters)
     peak, peak_kind = peak_hbm()
-    up_s, up_bytes, up_name = kernel_roofline(times, n, nt, B, 5)
-    dn_s, dn_bytes, dn_name = kernel_roofline(times, n, nt, B, 4)
-    traffic, traffic_dn = None, None
+    up_s, up_bytes, up_name = kernel_roofline(times, n, nt, B, 7)
+    l1 = {}
+    for kind, label in ((5, "up"), (1, "down")):
+        ks, kb, kn = kernel_roofline(times, n // 2, nt, B, kind)
+        if ks:
+            l1[label] = {"kernel": kn, "bytes_per_launch": kb, "launch_s": ks, "achieved": kb / ks / 1e9,
+                         "frac": kb / ks / 1e9 / peak}
+    traffic = None
     try:
         with open(PROFILE_SUMMARY) as fh:
             prof = json.load(fh).get(args.workload, {})
-        traffic = prof.get("up2_dram_bytes_per_launch")
-        traffic_dn = prof.get("downnorm_dram_bytes_per_launch")
+        traffic = prof.get("fused_dram_bytes_per_launch")
     except Exception:
         pass
 
@@ -361,16 +369,15 @@ def run_gpu_arm(args, w):
             "wall_s_to_1e-8": ms * 1e-3, "iterations": sorted(set(i for r in iters for i in r)),
             "roofline": {"bound": "hbm", "achieved": up_bytes / up_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": up_bytes / up_s / 1e9 / peak, "traffic": traffic,
-                         "kernel": "finest-level fused up pass (prolong-add + nu2 sweeps, pre-sweeps "
-                                   "recomputed; K_UP2), whole batch: " + up_name,
+                         "kernel": "finest-level fused pass: up pass of cycle k (pre-sweeps recomputed, "
+                                   "prolong-add, nu2 sweeps) + down pass of cycle k+1 (norm leaves, nu1 "
+                                   "sweeps, residual, restriction); K_UP2DOWN, whole batch: " + up_name,
                          "bytes_per_launch": up_bytes, "launch_s": up_s,
                          "timing": "CUDA events on the launch stream around the plan's own launches "
                                    "(tmg_trace_enable), one solve after the timed region",
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "frac_of_nominal_8TBs": up_bytes / up_s / 1e9 / 8000.0,
-                         "down_pass": {"kernel": dn_name, "bytes_per_launch": dn_bytes, "launch_s": dn_s,
-                                       "achieved": dn_bytes / dn_s / 1e9, "frac": dn_bytes / dn_s / 1e9 / peak,
-                                       "traffic": traffic_dn}},
+                         "level1_passes": l1},
             "e2e": {"value": dof_e2e / e2e_time, "unit": UNIT,
                     "h2d_bytes_per_step": B * n * nt * 8, "d2h_bytes_per_step": B * n * nt * 8,
                     "steps": e2e_steps, "path": "DevicePlan.solve_host -> C ABI tmg_plan_solve_host with pinned "
@@ -380,10 +387,13 @@ def run_gpu_arm(args, w):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
-        # whole-cycle HBM fraction: ~13 n_t * 8 algorithmic bytes per finest slab
-        # per V-cycle, summed over every problem-cycle of the run
+        # whole-cycle HBM fraction over every problem-cycle of the run: this
+        # design moves 8 n_t 8 B per finest slab per V-cycle (finest fused pass
+        # 4.0 + levels >= 1 (1.5 + 2.5) / 2 / (1 - 1/2)); SURVEY 8(d)'s model
+        # (every pass stores u, separate passes) is 13 n_t 8 B
         cycles = sum(sum(r) for r in iters)
-        line["cycle_hbm_frac"] = (13 * nt * 8 * n * cycles) / elapsed / 1e9 / peak
+        line["cycle_hbm_frac"] = (8 * nt * 8 * n * cycles) / elapsed / 1e9 / peak
+        line["cycle_hbm_frac_survey_model"] = (13 * nt * 8 * n * cycles) / elapsed / 1e9 / peak
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -365,6 +365,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     std::vector<int> pk;  // LU permutation pattern per level
     LevelC<T, NT> *d_levels = nullptr;
     std::vector<T *> uA, uB, fl, halo;
+    T *halo0_alt = nullptr;  // second finest-level halo buffer (K_UP2DOWN alternates them)
     bool up2 = false;  // up passes recompute the pre-sweeps (nu1 == nu2): no stored pre-smoothed u
     int tl = 0;                 // first tail level
     bool tail_smem = true;
@@ -405,6 +406,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         for (auto p : uB) cudaFree(p);
         for (auto p : fl) cudaFree(p);
         for (auto p : halo) cudaFree(p);
+        cudaFree(halo0_alt);
         cudaFree(d_levels);
         if (d_trace) {
             std::vector<unsigned long long> tr(6 * MAXLEV);
@@ -521,6 +523,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             for (int l = 0; l < tl; ++l) {
                 StreamArgs<T> a = level_args(l);
                 CK(cudaMalloc(&halo[l], sizeof(T) * (size_t)B * a.chunks * ROWW * NT + 16));
+                if (l == 0) CK(cudaMalloc(&halo0_alt, sizeof(T) * (size_t)B * a.chunks * ROWW * NT + 16));
             }
         }
         if (leaf_rows0) {
@@ -610,7 +613,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     // coarse-grid correction of level l and its up pass (norm_up: the up pass
     // also produces the norm of its output -- used when the down pass cannot)
-    int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s, bool first_visit = true)
+    int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s, bool first_visit = true,
+                     bool fuse_next_down = false)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
         if (l + 1 == tl) {
@@ -641,12 +645,22 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             a.halo = halo[l];
             a.active = d_active;
             a.flags = SF_PROLONG | SF_WRITE_U | (zero ? SF_ZERO_GUESS : 0);
-            if (norm_up) {
+            if (norm_up || fuse_next_down) {
                 a.flags |= SF_NORM_LEAF;
                 a.leaf_out = leaves;
             }
+            int kind = norm_up ? K_UP2NORM : K_UP2;
+            if (fuse_next_down) {
+                // ... and the next cycle's finest down pass on the same rows
+                kind = K_UP2DOWN;
+                a.flags |= SF_RESTRICT;
+                a.fc = fl[1];
+                a.halo_alt = halo0_alt;
+                a.iters = &d_st[0].iters;
+                a.iters_stride = (int)(sizeof(ProbState) / sizeof(int));
+            }
             if (tma_ok<T, NT>(a, true)) a.flags |= SF_TMA;
-            CKR((launch_stream<T, NT>(L[l], a, o.nu2, norm_up ? K_UP2NORM : K_UP2, pk[l], SP, s)));
+            CKR((launch_stream<T, NT>(L[l], a, o.nu2, kind, pk[l], SP, s)));
             ++kernels_per_cycle;
             return 0;
         }
@@ -705,6 +719,16 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     // Measured on config 3: 128.3 vs 131.1 ms per solve, config 2 ~1-2 %.
     bool norm_up2() const { return up2 && leaf_rows0 > 0 && SP && norm_up_env(); }
     bool norm_in() const { return leaf_rows0 > 0 && SP && !norm_up2(); }
+    // K_UP2DOWN (default with the up2 scheme; TMG_NO_FUSE=1 keeps the two passes)
+    bool fuse_up_down() const
+    {
+        static int v = -1;
+        if (v < 0) {
+            const char *e = getenv("TMG_NO_FUSE");
+            v = (e && *e && *e != '0') ? 0 : 1;
+        }
+        return up2 && v == 1 && tl >= 1;
+    }
     static bool norm_up_env()
     {
         static int v = -1;
@@ -738,7 +762,11 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                       cudaGraphConditionalHandle h = 0, bool use_h = false)
     {
         kernels_per_cycle = 0;
-        if (norm && norm_in()) {
+        if (norm && norm_in() && fuse_up_down()) {
+            // rest of this cycle; its finest up pass fused with the NEXT cycle's
+            // finest down pass (whose first sweep yields ||f - L u||)
+            CKR(enqueue_rest(0, f, u, false, s, true, true));
+        } else if (norm && norm_in()) {
             // rest of this cycle, then the NEXT cycle's finest down pass, whose
             // first sweep yields ||f - L u|| of this cycle's result
             CKR(enqueue_rest(0, f, u, false, s));

@@ -76,6 +76,7 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
     case K_DOWNNORM: return by_perm<T, NT, K_DOWNNORM>(L, a, nu, perm, s);
     case K_UP2: return by_perm<T, NT, K_UP2>(L, a, nu, perm, s);
     case K_UP2NORM: return by_perm<T, NT, K_UP2NORM>(L, a, nu, perm, s);
+    case K_UP2DOWN: return by_perm<T, NT, K_UP2DOWN>(L, a, nu, perm, s);
     }
     return -1;
 }

@@ -45,11 +45,13 @@ constexpr int SW_LEAF_BATCH = 4;    // numpy leaves reduced together (one per 8 
 // latency-bound, at this occupancy.
 template <typename T, int NT> struct CtaShape {
     static constexpr bool PAIR = slabs_per_lane<T, NT>() == 2;
-    static constexpr int WARPS = PAIR ? TMG_P2_WARPS : 8;
-    static constexpr int MINB = PAIR ? TMG_P2_MINB : 2;
+    // two fp64 slabs of n_t >= 3 per lane need > 128 registers: one CTA per SM
+    static constexpr bool WIDE = PAIR && sizeof(T) == 8 && NT >= 3;
+    static constexpr int WARPS = WIDE ? 8 : PAIR ? TMG_P2_WARPS : 8;
+    static constexpr int MINB = WIDE ? 1 : PAIR ? TMG_P2_MINB : 2;
     // shared memory per CTA that keeps MINB CTAs resident (227 KB per SM,
     // 1 KB reserved per CTA)
-    static constexpr size_t CAP = PAIR ? (TMG_P2_MINB >= 3 ? 72 * 1024 : 104 * 1024) : 110 * 1024;
+    static constexpr size_t CAP = WIDE ? 200 * 1024 : PAIR ? (TMG_P2_MINB >= 3 ? 72 * 1024 : 104 * 1024) : 110 * 1024;
 };
 
 enum StreamFlags : int {
@@ -72,7 +74,15 @@ enum StreamFlags : int {
 // reading a stored pre-smoothed iterate -- the down pass then writes no u.
 // K_UP2NORM: K_UP2 that also returns the residual norm of its OUTPUT (the
 // stopping test of the cycle it ends, multigrid.py:447-459)
-enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM = 4, K_UP2 = 5, K_UP2NORM = 6 };
+// K_UP2DOWN: the finest up pass of cycle k FUSED with the finest down pass of
+// cycle k+1 (K_UP2 then K_DOWNNORM on the same rows in registers): u is read
+// and f read once for both, the new iterate stored once; the down part is
+// speculative exactly like the separate K_DOWNNORM was (discarded when the
+// stopping test ends the solve).  Halo rows alternate between two buffers by
+// cycle parity (the up part reads the previous cycle's, the down part writes
+// the next one's).
+enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM = 4, K_UP2 = 5, K_UP2NORM = 6,
+                  K_UP2DOWN = 7 };
 
 template <typename T> struct StreamArgs {
     const T *f;
@@ -83,6 +93,9 @@ template <typename T> struct StreamArgs {
     T *r_out;
     T *halo;               // [batch][chunks][32*P][NT]: each chunk's last row of the ORIGINAL
                            // iterate (written by down passes, read by K_UP2 warm-up rows)
+    T *halo_alt;           // K_UP2DOWN: the second halo buffer
+    const int *iters;      // K_UP2DOWN: per-problem cycle counter (parity picks the halo buffer)
+    int iters_stride;      // in ints
     double *sq_out;
     double *leaf_out;
     const int *active;
@@ -154,7 +167,8 @@ template <int KIND> struct KindProlongs {
     static constexpr bool value = KIND != K_DOWN && KIND != K_DOWNNORM;
 };
 template <int KIND> struct KindLeaf {
-    static constexpr bool value = KIND == K_GENERIC || KIND == K_UPNORM || KIND == K_DOWNNORM || KIND == K_UP2NORM;
+    static constexpr bool value =
+        KIND == K_GENERIC || KIND == K_UPNORM || KIND == K_DOWNNORM || KIND == K_UP2NORM || KIND == K_UP2DOWN;
 };
 
 // vector load/store of one lane's P*NT consecutive elements (16-byte pieces
@@ -255,9 +269,12 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                               : KIND == K_DOWNNORM ? (SF_RESTRICT | SF_WRITE_U | SF_NORM_LEAF)
                               : KIND == K_UP2 ? (SF_PROLONG | SF_WRITE_U)
                               : KIND == K_UP2NORM ? (SF_PROLONG | SF_WRITE_U | SF_NORM_LEAF)
+                              : KIND == K_UP2DOWN ? (SF_PROLONG | SF_WRITE_U | SF_RESTRICT | SF_NORM_LEAF)
                                                   : 0;
-    // pre-sweeps recomputed before the prolongation (K_UP2, K_UP2NORM)
-    static constexpr int NPRE = (KIND == K_UP2 || KIND == K_UP2NORM) ? NU : 0;
+    // pre-sweeps recomputed before the prolongation (K_UP2, K_UP2NORM, K_UP2DOWN)
+    static constexpr int NPRE = (KIND == K_UP2 || KIND == K_UP2NORM || KIND == K_UP2DOWN) ? NU : 0;
+    // sweeps of the next cycle's down pass after the up pass (K_UP2DOWN; nu1 == nu2)
+    static constexpr int NPOST = KIND == K_UP2DOWN ? NU : 0;
     // norm of the pass's input (K_DOWNNORM) rather than of its output
     static constexpr bool NORM_IN = KIND == K_DOWNNORM && NU > 0;
     static constexpr int P = slabs_per_lane<T, NT>();
@@ -272,13 +289,14 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     static constexpr bool RREG = P == 1 && NT * NT * sizeof(T) <= 64;
     T Rm[RREG ? NT * NT : 1];
     const T *Rs;
-    C carry[NPRE + NU + 1];  // lane 0: predecessor data of the next row, per sweep
+    C carry[NPRE + NU + NPOST + 1];  // lane 0: predecessor data of the next row, per sweep
     T *leafbuf;              // per-warp numpy leaf buffer (SF_NORM_LEAF)
     int leaf_q;              // rows buffered in leafbuf
     long long leaf0;         // index of the first buffered leaf
     long long nc;
     bool write_u;            // the pass stores u (u_out given)
     bool vec_out;            // u_out rows are 16-byte aligned (vector stores)
+    T *halo_w;               // K_UP2DOWN: this lane's slot of the chunk's halo row (last row only)
 
     __device__ __forceinline__ bool has(int f) const
     {
@@ -399,9 +417,44 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                 sweep_j<T, NT, SPARSE, PERM, P>(L, u, f, prev, hp);
             }
         }
+        if constexpr (NPOST > 0) {
+            // the up pass is complete: store this cycle's result (and, on the
+            // chunk's last row, its halo for the next cycle's up pass)
+            if (!warm && write_u) {
+                if (INTERIOR && vec_out) {
+                    store_lane<T, NT, P>(uo, u);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (valid[q]) store_slab<T, NT>(uo + q * NT, u[q]);
+                }
+            }
+            if (!warm && halo_w) store_lane<T, NT, P>(halo_w, u);
+            // the next cycle's down pass; its first sweep's residual is the
+            // stopping norm of the result just stored
+#pragma unroll
+            for (int k = 0; k < NPOST; ++k) {
+                C prev[P];
+                exchange(u, NPRE + NU + k, prev);
+                if (k == 0) {
+                    T y[P][NT];
+#pragma unroll
+                    for (int q = 0; q < P; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], prev[q], hp[q], y[q]);
+                    if (!warm) {
+                        T r[P][NT];
+#pragma unroll
+                        for (int q = 0; q < P; ++q) unpermute<T, NT, PERM>(L, y[q], r[q]);
+                        leaf_row(r, row_idx, b);
+                    }
+                    finish_j<T, NT, P>(L, u, y);
+                } else {
+                    sweep_j<T, NT, SPARSE, PERM, P>(L, u, f, prev, hp);
+                }
+            }
+        }
         if (need_r()) {
             C prev[P];
-            exchange(u, NPRE + NU, prev);
+            exchange(u, NPRE + NU + NPOST, prev);
             if (!warm) {
                 T r[P][NT];
 #pragma unroll
@@ -438,10 +491,10 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                     for (int q = 0; q < P; ++q)
                         if (valid[q]) a.sq_out[(size_t)b * a.n + slab0 + q] = (double)sqnorm<T, NT>(r[q]);
                 }
-                if (!NORM_IN && has(SF_NORM_LEAF)) leaf_row(r, row_idx, b);
+                if (!NORM_IN && NPOST == 0 && has(SF_NORM_LEAF)) leaf_row(r, row_idx, b);
             }
         }
-        if (has(SF_WRITE_U) && !warm && write_u) {
+        if (NPOST == 0 && has(SF_WRITE_U) && !warm && write_u) {
             if (INTERIOR && vec_out) {
                 store_lane<T, NT, P>(uo, u);
             } else {
@@ -513,7 +566,18 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         }
     }
 #pragma unroll
-    for (int k = 0; k <= S::NPRE + NU; ++k) cpl_zero(st.carry[k]);
+    for (int k = 0; k <= S::NPRE + NU + S::NPOST; ++k) cpl_zero(st.carry[k]);
+    st.halo_w = nullptr;
+    // halo buffers: K_UP2DOWN alternates them by the problem's cycle parity
+    T *halo_in = a.halo, *halo_next = nullptr;
+    if constexpr (S::NPOST > 0) {
+        if (a.iters[(size_t)b * a.iters_stride] & 1) {
+            halo_in = a.halo_alt;
+            halo_next = a.halo;
+        } else {
+            halo_next = a.halo_alt;
+        }
+    }
     st.leaf_q = 0;
     st.leaf0 = 0;
 
@@ -572,7 +636,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         const long long wr = row0 - 1;
         load_row_gen(wr, u, f, uc, !zero_guess && S::NPRE == 0);
         if (S::NPRE > 0 && !zero_guess)  // the neighbour chunk may already have overwritten this row
-            load_lane<T, NT, P>(a.halo + ((size_t)b * a.chunks + chunk - 1) * Lay::ROW + lofs * NT, u);
+            load_lane<T, NT, P>(halo_in + ((size_t)b * a.chunks + chunk - 1) * Lay::ROW + lofs * NT, u);
         if (wr > 0) st.template row<true>(u, f, uc, wr * W + lofs, wr, true, b, nullptr, nullptr, zero_guess);
         else st.template row<false>(u, f, uc, wr * W + lofs, wr, true, b, nullptr, nullptr, zero_guess);
     }
@@ -614,6 +678,10 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
                 // the chunk's last row: the next chunk's up-pass warm-up input
                 store_lane<T, NT, P>(a.halo + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT, u);
             }
+            if constexpr (S::NPOST > 0)
+                st.halo_w = (rr == rows - 1 && chunk + 1 < a.chunks)
+                                ? halo_next + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT
+                                : nullptr;
             if (interior)
                 st.template row<true>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, zero_guess);
             else

@@ -19,7 +19,10 @@ constexpr int MAXLEV = 48;
 // streaming kernels: consecutive slabs owned by one lane (a row is 32*P slabs).
 // Two slabs give each lane two independent dependency chains and make the
 // restriction pairs lane-local; larger fp64 blocks would spill.
-template <typename T, int NT> constexpr int slabs_per_lane() { return (NT <= 2 || sizeof(T) == 4) ? 2 : 1; }
+#ifndef TMG_WIDE_FP64
+#define TMG_WIDE_FP64 0  // experiment: two-slab lanes for n_t >= 3 fp64 too (one 8-warp CTA per SM)
+#endif
+template <typename T, int NT> constexpr int slabs_per_lane() { return (NT <= 2 || sizeof(T) == 4 || TMG_WIDE_FP64) ? 2 : 1; }
 // fine slabs per TMA ring stage (a multiple of the row): the per-stage work
 // (mbarrier wait, proxy fence, refill) is ~80 instructions, so two-slab lanes
 // take two 64-slab rows per stage; one-slab lanes keep 2 rows of 32 slabs

@@ -2,9 +2,9 @@
 # GPU-box profiling recipe for the headline (BASELINE config 3), one GPU:
 #   1. bench.py (the JSON line, CPU baseline included)
 #   2. ncu launch list of bench.py (gpu__time_duration per launch, serialised)
-#   3. ncu --set full of the two dominant kernels of one solve
-#      (finest-level fused down pass with norm leaves, K_DOWNNORM; finest-level
-#      up pass, K_UP2), located from a launch list of scripts/ncu_target.py
+#   3. ncu --set full of the two dominant kernels of one solve (the finest
+#      level's fused up / next-down pass, K_UP2DOWN; the level-1 up pass,
+#      K_UP2), located from a launch list of scripts/ncu_target.py
 # Usage (from the repo root, under gpurun):  bash scripts/profile_round.sh [tag]
 set -u
 TAG=${1:-r01}
@@ -19,7 +19,7 @@ echo "launch list rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/${TAG}_launches_target.csv python scripts/ncu_target.py > $OUT/${TAG}_ncu_target.log 2>&1
 echo "target launch list rc=$?"
-# index (among launches of the same kernel name) of the longest K_DOWNNORM and K_UP2 launch
+# index (among launches of the same kernel name) of the longest K_UP2DOWN (finest, fused) and K_UP2 (level 1) launch
 read SKIP4 SKIP5 < <(python - "$OUT/${TAG}_launches_target.csv" <<'EOF'
 import csv, sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
@@ -29,12 +29,12 @@ norm = lambda k: k.replace("(int)", "").replace("(bool)", "").replace("true", "1
 def best(tag):
     seq = [float(r[vi].replace(",", "")) for r in rows if tag in norm(r[ki])]
     return max(range(len(seq)), key=lambda i: seq[i]) if seq else 0
-print(best("stream_kernel<double, 2, 1, 1, 4,"), best("stream_kernel<double, 2, 1, 1, 5,"))
+print(best("stream_kernel<double, 2, 1, 1, 7,"), best("stream_kernel<double, 2, 1, 1, 5,"))
 EOF
 )
 echo "skip kind4=$SKIP4 kind5=$SKIP5"
-for K in 4 5; do
-    S=$([ $K = 4 ] && echo $SKIP4 || echo $SKIP5)
+for K in 7 5; do
+    S=$([ $K = 7 ] && echo $SKIP4 || echo $SKIP5)
     timeout 900 ncu --set full --import-source on --clock-control none \
         --kernel-name-base demangled \
         -k "regex:stream_kernel<double, (\\(int\\))?2, (\\(int\\))?1, (\\(bool\\))?(1|true), (\\(int\\))?$K," --launch-skip $S --launch-count 1 \

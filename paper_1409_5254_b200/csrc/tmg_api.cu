@@ -274,18 +274,20 @@ int chunk_rows(long long n, long long batch, int leaf_rows, int w, int stage)
 {
     const long long rows = (n + w - 1) / w;
     // TMG_CHUNK_WAVES / TMG_CHUNK_MIN: tuning overrides (default 2 waves of
-    // 16 resident warps per SM, chunks of >= 2 rows; 2 waves measured best on
-    // the latency-bound 2^20-slab levels, large batches hit the 128-row cap)
-    static int waves = -1, rmin = -1;
+    // 16 resident warps per SM, chunks of 2..64 rows; 2 waves measured best on
+    // the latency-bound 2^20-slab levels, large batches hit the 64-row cap)
+    static int waves = -1, rmin = -1, rmax = -1;
     if (waves < 0) {
         const char *e = getenv("TMG_CHUNK_WAVES");
         waves = e ? std::max(1, atoi(e)) : 2;
         const char *m = getenv("TMG_CHUNK_MIN");
         rmin = m ? std::max(1, atoi(m)) : 2;
+        const char *x = getenv("TMG_CHUNK_MAX");
+        rmax = x ? std::max(rmin, atoi(x)) : 64;  // 32-96 measured ~1 % better than 128 on config 3
     }
     const long long target_warps = (long long)sm_count() * 16 * waves;
     long long r = (rows * batch) / std::max(1LL, target_warps);
-    r = std::max((long long)rmin, std::min(128LL, r));
+    r = std::max((long long)rmin, std::min((long long)rmax, r));
     // a multiple of the ring stage (stage_slabs) and of the norm leaf
     const int g = stage / w;
     const int q = std::lcm(g, std::max(leaf_rows, 1));

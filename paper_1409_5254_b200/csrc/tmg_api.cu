@@ -368,6 +368,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     LevelC<T, NT> *d_levels = nullptr;
     std::vector<T *> uA, uB, fl, halo;
     T *halo0_alt = nullptr;  // second finest-level halo buffer (K_UP2DOWN alternates them)
+    T *fl1_alt = nullptr;    // second level-1 right-hand side (vertical fusion alternates them)
     bool up2 = false;  // up passes recompute the pre-sweeps (nu1 == nu2): no stored pre-smoothed u
     int tl = 0;                 // first tail level
     bool tail_smem = true;
@@ -409,6 +410,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         for (auto p : fl) cudaFree(p);
         for (auto p : halo) cudaFree(p);
         cudaFree(halo0_alt);
+        cudaFree(fl1_alt);
         cudaFree(d_levels);
         if (d_trace) {
             std::vector<unsigned long long> tr(6 * MAXLEV);
@@ -527,6 +529,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                 CK(cudaMalloc(&halo[l], sizeof(T) * (size_t)B * a.chunks * ROWW * NT + 16));
                 if (l == 0) CK(cudaMalloc(&halo0_alt, sizeof(T) * (size_t)B * a.chunks * ROWW * NT + 16));
             }
+            if (tl >= 2 && ROWW == 64 && sizeof(T) == 8 && n[0] % 128 == 0)
+                CK(cudaMalloc(&fl1_alt, sizeof(T) * (size_t)B * n[1] * NT + 16));
         }
         if (leaf_rows0) {
             nleaves = n[0] / ((long long)ROWW * leaf_rows0);
@@ -591,11 +595,17 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     // down pass of level l (nu1 sweeps + residual + restriction); with_norm:
     // also the numpy-order norm leaves of its INPUT (finest level, solve mode)
-    int enqueue_down(int l, const void *f0, void *u0, bool first_visit, bool with_norm, cudaStream_t s)
+    int enqueue_down(int l, const void *f0, void *u0, bool first_visit, bool with_norm, cudaStream_t s,
+                     bool f_by_parity = false)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
         StreamArgs<T> a = up2 ? level_args(l) : stream_args<T, NT>(n[l], B, with_norm ? leaf_rows0 : 1);
         a.f = fL;
+        if (f_by_parity) {  // vertical fusion: level 1's f alternates by cycle parity
+            a.f_alt = fl1_alt;
+            a.iters = &d_st[0].iters;
+            a.iters_stride = (int)(sizeof(ProbState) / sizeof(int));
+        }
         const bool zero = (l > 0) && first_visit;
         a.u_in = l == 0 ? (const T *)u0 : (zero ? nullptr : uA[l]);
         a.u_out = up2 ? nullptr : uB[l];
@@ -616,7 +626,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     // coarse-grid correction of level l and its up pass (norm_up: the up pass
     // also produces the norm of its output -- used when the down pass cannot)
     int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s, bool first_visit = true,
-                     bool fuse_next_down = false)
+                     bool fuse_next_down = false, bool skip_up = false)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
         if (l + 1 == tl) {
@@ -634,6 +644,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         } else {
             for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s));
         }
+        if (skip_up) return 0;  // level 1 under the vertical fusion: its up pass runs inside the finest pass
         if (up2 && (!norm_up || (l == 0 && norm_up2()))) {
             // prolong-add + post-sweeps, the pre-sweeps recomputed from the
             // level's original iterate (read in place; warm-ups from the halo);
@@ -721,6 +732,17 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     // Measured on config 3: 128.3 vs 131.1 ms per solve, config 2 ~1-2 %.
     bool norm_up2() const { return up2 && leaf_rows0 > 0 && SP && norm_up_env(); }
     bool norm_in() const { return leaf_rows0 > 0 && SP && !norm_up2(); }
+    // vertical fusion (level-1 up pass inside the fused finest pass; TMG_NO_VFUSE=1 disables)
+    bool vfuse(const void *f, const void *u) const
+    {
+        static int v = -1;
+        if (v < 0) {
+            const char *e = getenv("TMG_NO_VFUSE");
+            v = (e && *e && *e != '0') ? 0 : 1;
+        }
+        return v == 1 && fuse_up_down() && fl1_alt && o.gamma == 1 && tl >= 2 && pk[0] == pk[1] &&
+               aligned16(f) && aligned16(u) && aligned16(fl[1]) && aligned16(fl1_alt) && aligned16(uA[2]);
+    }
     // K_UP2DOWN (default with the up2 scheme; TMG_NO_FUSE=1 keeps the two passes)
     bool fuse_up_down() const
     {
@@ -764,7 +786,36 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                       cudaGraphConditionalHandle h = 0, bool use_h = false)
     {
         kernels_per_cycle = 0;
-        if (norm && norm_in() && fuse_up_down()) {
+        if (norm && norm_in() && vfuse(f, u)) {
+            // vertical fusion: level 1's down pass (f_1 by parity), the coarser
+            // levels, then ONE finest pass = level-1 up pass + finest up pass +
+            // the next cycle's finest down pass
+            CKR(enqueue_down(1, f, u, true, false, s, true));
+            CKR(enqueue_rest(1, f, u, false, s, true, false, true));
+            StreamArgs<T> a = level_args(0);
+            a.f = (const T *)f;
+            a.u_in = (const T *)u;
+            a.u_out = (T *)u;
+            a.uc = uA[2];
+            a.f1 = fl[1];
+            a.f1_alt = fl1_alt;
+            a.halo = halo[0];
+            a.halo_alt = halo0_alt;
+            a.iters = &d_st[0].iters;
+            a.iters_stride = (int)(sizeof(ProbState) / sizeof(int));
+            a.active = d_active;
+            a.leaf_out = leaves;
+            a.flags = SF_PROLONG | SF_WRITE_U | SF_RESTRICT | SF_NORM_LEAF | SF_TMA;
+            StreamArgs<T> a1 = a;
+            a1.n = n[1];
+            a1.flags = SF_PROLONG | SF_WRITE_U | SF_ZERO_GUESS;
+            const int rc = stream_v_launch<T, NT>(L[0], L[1], a, a1, o.nu2, pk[0], s);
+            if (rc < 0) return fail(TMG_E_UNSUPPORTED, "vertical fusion unavailable");
+            if (rc > 0) return fail(rc, "stream_kernel_v: %s", cudaGetErrorString((cudaError_t)rc));
+            CK_LAUNCH("stream_kernel_v");
+            trace_mark("stream_kernel_v (level-1 up + finest up + next finest down)", s);
+            ++kernels_per_cycle;
+        } else if (norm && norm_in() && fuse_up_down()) {
             // rest of this cycle; its finest up pass fused with the NEXT cycle's
             // finest down pass (whose first sweep yields ||f - L u||)
             CKR(enqueue_rest(0, f, u, false, s, true, true));

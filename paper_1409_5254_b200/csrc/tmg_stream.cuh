@@ -86,6 +86,9 @@ enum Kind : int { K_GENERIC = 0, K_DOWN = 1, K_UP = 2, K_UPNORM = 3, K_DOWNNORM 
 
 template <typename T> struct StreamArgs {
     const T *f;
+    const T *f_alt;        // K_DOWN at level 1 under the vertical fusion: f double-buffered by cycle parity
+    const T *f1;           // stream_kernel_v: level-1 right-hand side, buffer A (parity 0 reads A, writes B)
+    T *f1_alt;             // stream_kernel_v: buffer B
     const T *u_in;
     T *u_out;
     const T *uc;
@@ -292,6 +295,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     C carry[NPRE + NU + NPOST + 1];  // lane 0: predecessor data of the next row, per sweep
     T *leafbuf;              // per-warp numpy leaf buffer (SF_NORM_LEAF)
     int leaf_q;              // rows buffered in leafbuf
+    int lb = LB;             // leaves per flush (the buffer's capacity)
     long long leaf0;         // index of the first buffered leaf
     long long nc;
     bool write_u;            // the pass stores u (u_out given)
@@ -339,7 +343,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
 #pragma unroll
         for (int q = 0; q < P; ++q) sq[q] = sqnorm<T, NT>(r[q]);
         vstore<T, P>(leafbuf + leaf_q * W + lane * P, sq);
-        if (++leaf_q == LB * a.leaf_rows) leaf_flush(b);
+        if (++leaf_q == lb * a.leaf_rows) leaf_flush(b);
     }
 
     // predecessor data of the row's P slabs at sweep k: the lane's own earlier
@@ -539,7 +543,8 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     const bool prolong = WITH_C && st.has(SF_PROLONG);
     const int lofs = lane * P;  // this lane's first slab within a row
 
-    const T *fb = a.f + (size_t)b * n * NT;
+    const T *fsrc = (a.f_alt && (a.iters[(size_t)b * a.iters_stride] & 1)) ? a.f_alt : a.f;
+    const T *fb = fsrc + (size_t)b * n * NT;
     const T *ub = zero_guess ? nullptr : a.u_in + (size_t)b * n * NT;
     const T *ucb = prolong ? a.uc + (size_t)b * st.nc * NT : nullptr;
 
@@ -691,6 +696,184 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         }
     }
     if (KindLeaf<KIND>::value && st.has(SF_NORM_LEAF) && st.leaf_q > 0) st.leaf_flush(b);
+}
+
+
+// ---------------------------------------------------------------------------
+// Vertical fusion at the finest level (two-slab lanes): the level-1 up pass
+// (zero original iterate: omega LU^-1 f pre-sweep, prolong-add of u_2, nu2
+// sweeps) runs INSIDE the fused finest pass.  Per ring stage: one coarse row
+// of level 1 (64 slabs) is computed into a per-warp shared-memory row, then
+// the two fine rows it covers run the K_UP2DOWN row with their u_c taken from
+// that row -- so u_1 is never stored nor re-read.  f_1 alternates between two
+// buffers by cycle parity (this cycle's is read here and by nothing later;
+// the next cycle's is written here and read by the level-1 down pass), like
+// the halo rows.  Warm-up: the coarse row before the chunk, then the fine row
+// before it (its u_c is that coarse row's exact second half).
+template <typename T, int NT> struct RowLayoutV {
+    static constexpr int W = 64;
+    static constexpr int ROW = W * NT;       // elements of a 64-slab row (fine or coarse)
+    static constexpr int HALF = ROW / 2;
+    static constexpr int OFF_F = 2 * ROW;    // stage: u0 rows | f0 rows | f1 row | u2 half row
+    static constexpr int OFF_F1 = 4 * ROW;
+    static constexpr int OFF_C2 = 5 * ROW;
+    static constexpr int STAGE = 5 * ROW + HALF;
+    static constexpr int ST = 2;
+    static constexpr int LB = 2;             // numpy leaves per flush (smem budget)
+    static constexpr int LEAFBUF = LB * 128;
+    static constexpr int WARPS = CtaShape<T, NT>::WARPS;
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + LEAFBUF);
+    static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
+    static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
+};
+
+template <typename T, int NT, int NU, bool SPARSE, int PERM>
+__global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::MINB)
+    stream_kernel_v(const __grid_constant__ LevelC<T, NT> L, const __grid_constant__ LevelC<T, NT> L1,
+                    const __grid_constant__ StreamArgs<T> a, const __grid_constant__ StreamArgs<T> a1)
+{
+    using Lay = RowLayoutV<T, NT>;
+    using S = Streamer<T, NT, NU, SPARSE, K_UP2DOWN, PERM>;
+    using S1 = Streamer<T, NT, NU, SPARSE, K_UP2, PERM>;
+    static_assert(S::P == 2, "vertical fusion needs two-slab lanes");
+    constexpr int P = 2, W = 64;
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const long long gw = (long long)blockIdx.x * Lay::WARPS + warp;
+    if (gw >= (long long)a.batch * a.chunks) return;
+    const int b = (int)(gw / a.chunks);
+    const long long chunk = gw - (long long)b * a.chunks;
+    if (a.active && !a.active[b]) return;
+
+    const long long n = a.n, n1 = n >> 1, n2 = n >> 2;
+    S st{L, a, lane, a.flags};
+    st.nc = n1;
+    S1 s1{L1, a1, lane, a1.flags};
+    s1.nc = n2;
+    const long long row0 = chunk * a.rows_per_chunk;          // even; every row full (n % 128 == 0)
+    const int rows = (int)min((long long)a.rows_per_chunk, n / W - row0);
+    const int ngroups = rows >> 1;
+    const int lofs = lane * P;
+    const bool par = a.iters[(size_t)b * a.iters_stride] & 1;
+    T *halo_in = par ? a.halo_alt : a.halo;
+    T *halo_next = par ? a.halo : a.halo_alt;
+    const T *f1b = (par ? a.f1_alt : a.f1) + (size_t)b * n1 * NT;   // this cycle's f_1
+    T *fcb = (par ? (T *)a.f1 : a.f1_alt) + (size_t)b * n1 * NT;     // the next cycle's f_1
+    const T *fb = a.f + (size_t)b * n * NT;
+    const T *ub = a.u_in + (size_t)b * n * NT;
+    const T *u2b = a.uc + (size_t)b * n2 * NT;
+
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * Lay::ST;
+    unsigned char *wbase = smem + Lay::BAR_BYTES + (size_t)warp * Lay::BYTES_PER_WARP;
+    st.leafbuf = reinterpret_cast<T *>(wbase);
+    st.lb = Lay::LB;
+    T *u1row = reinterpret_cast<T *>(wbase) + Lay::LEAFBUF;
+    T *ring = u1row + Lay::ROW;
+#pragma unroll
+    for (int k = 0; k <= S::NPRE + NU + S::NPOST; ++k) cpl_zero(st.carry[k]);
+#pragma unroll
+    for (int k = 0; k <= S1::NPRE + NU; ++k) cpl_zero(s1.carry[k]);
+    st.leaf_q = 0;
+    st.leaf0 = 0;
+    st.halo_w = nullptr;
+    st.write_u = true;
+    st.vec_out = true;
+    s1.leaf_q = 0;
+    s1.leaf0 = 0;
+    s1.halo_w = nullptr;
+    s1.write_u = true;
+    s1.vec_out = true;
+    T *uo = a.u_out + ((size_t)b * n + (size_t)row0 * W + lofs) * NT;
+    T *fco = fcb + (((size_t)row0 * W + lofs) >> 1) * NT;
+    uint64_t pol = 0;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < Lay::ST; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        pol = policy_evict_first();
+    }
+    __syncwarp();
+    auto issue = [&](int g) {  // lane 0 only
+        T *stg = ring + (size_t)(g % Lay::ST) * Lay::STAGE;
+        uint64_t *bar = &bars[g % Lay::ST];
+        const long long s0 = (row0 + 2LL * g) * W;      // first fine slab of the stage
+        const long long c0 = s0 >> 1;                   // first level-1 slab
+        const uint32_t fine = (uint32_t)(2 * Lay::ROW * sizeof(T));
+        const uint32_t crow = (uint32_t)(Lay::ROW * sizeof(T));
+        const uint32_t chalf = (uint32_t)(Lay::HALF * sizeof(T));
+        mbar_expect_tx(bar, 2 * fine + crow + chalf);
+        bulk_g2s(stg, ub + s0 * NT, fine, bar, pol);
+        bulk_g2s(stg + Lay::OFF_F, fb + s0 * NT, fine, bar, pol);
+        bulk_g2s(stg + Lay::OFF_F1, f1b + c0 * NT, crow, bar, pol);
+        bulk_g2s(stg + Lay::OFF_C2, u2b + (c0 >> 1) * NT, chalf, bar, pol);
+    };
+    if (lane == 0)
+        for (int g = 0; g < ngroups && g < Lay::ST; ++g) issue(g);
+
+    // level-1 row cr into u1row (zero original iterate)
+    auto coarse_row = [&](long long cr, const T (&f1)[P][NT], const T (&u2)[NT]) {
+        T u[P][NT];
+#pragma unroll
+        for (int q = 0; q < P; ++q) zero_slab<T, NT>(u[q]);
+        if (cr > 0) s1.template row<true>(u, f1, u2, cr * W + lofs, cr, false, b, u1row + lofs * NT, nullptr, true);
+        else s1.template row<false>(u, f1, u2, cr * W + lofs, cr, false, b, u1row + lofs * NT, nullptr, true);
+        __syncwarp();
+    };
+
+    if (row0 > 0) {
+        // warm-up: the coarse row before the chunk, then the fine row before it
+        const long long cw = (row0 >> 1) - 1;
+        T f1[P][NT], u2[NT];
+#pragma unroll
+        for (int q = 0; q < P; ++q) load_slab_scalar<T, NT>(f1b + (cw * W + lofs + q) * NT, f1[q]);
+        load_slab_scalar<T, NT>(u2b + ((cw * W + lofs) >> 1) * NT, u2);
+        coarse_row(cw, f1, u2);
+        const long long wr = row0 - 1;
+        T u[P][NT], f[P][NT], uc[NT];
+#pragma unroll
+        for (int q = 0; q < P; ++q) load_slab_scalar<T, NT>(fb + (wr * W + lofs + q) * NT, f[q]);
+        load_lane<T, NT, P>(halo_in + ((size_t)b * a.chunks + chunk - 1) * Lay::ROW + lofs * NT, u);
+        load_slab<T, NT>(u1row + Lay::HALF + (lofs >> 1) * NT, uc);
+        st.template row<true>(u, f, uc, wr * W + lofs, wr, true, b, nullptr, nullptr, false);
+        __syncwarp();
+    }
+
+    for (int g = 0; g < ngroups; ++g) {
+        const T *stg = ring + (size_t)(g % Lay::ST) * Lay::STAGE;
+        mbar_wait(&bars[g % Lay::ST], (uint32_t)((g / Lay::ST) & 1));
+        {
+            T f1[P][NT], u2[NT];
+            load_lane<T, NT, P>(stg + Lay::OFF_F1 + lofs * NT, f1);
+            load_slab<T, NT>(stg + Lay::OFF_C2 + (lofs >> 1) * NT, u2);
+            coarse_row((row0 >> 1) + g, f1, u2);
+        }
+#pragma unroll 1
+        for (int qq = 0; qq < 2; ++qq) {
+            const int rr = 2 * g + qq;
+            const long long ridx = row0 + rr;
+            T u[P][NT], f[P][NT], uc[NT];
+            load_lane<T, NT, P>(stg + Lay::OFF_F + qq * Lay::ROW + lofs * NT, f);
+            load_lane<T, NT, P>(stg + qq * Lay::ROW + lofs * NT, u);
+            load_slab<T, NT>(u1row + qq * Lay::HALF + (lofs >> 1) * NT, uc);
+            if (qq == 1) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0 && g + Lay::ST < ngroups) issue(g + Lay::ST);
+            }
+            st.halo_w = (rr == rows - 1 && chunk + 1 < a.chunks)
+                            ? halo_next + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT
+                            : nullptr;
+            if (ridx > 0) st.template row<true>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, false);
+            else st.template row<false>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, false);
+            uo += Lay::ROW;
+            fco += Lay::HALF;
+        }
+        __syncwarp();  // every lane is done with u1row before the next coarse row overwrites it
+    }
+    if (st.leaf_q > 0) st.leaf_flush(b);
 }
 
 }  // namespace tmg

@@ -238,14 +238,19 @@ def live_kernel_times(plan, F, U, floors, eps, max_iters):
 # fused with the finest down pass of cycle k+1: reads u, f, u_c/2, writes u,
 # f_c/2; K_UP2 (5) at a coarse level (zero original iterate): reads f, u_c/2,
 # writes u; K_DOWN (1) at a coarse level (zero guess): reads f, writes f_c/2
-KIND_BYTES = {7: 4.0, 5: 2.5, 1: 1.5, 4: 2.5}
+# "v" = stream_kernel_v: K_UP2DOWN with the level-1 up pass fused in (vertical
+# fusion): reads u, f, f_1/2, u_2/4, writes u, f_c/2 -> 4.25
+KIND_BYTES = {"v": 4.25, 7: 4.0, 5: 2.5, 1: 1.5, 4: 2.5}
 
 
 def kernel_roofline(times, n, nt, B, kind):
     """(average launch seconds, algorithmic bytes per launch, description) of
-    the stream kernel of a kind at the level with n slabs per problem."""
+    the stream kernel of a kind at the level with n slabs per problem (kind
+    "v": the vertically fused finest pass)."""
     for name, (cnt, tot) in times.items():
-        if f"kind={kind}>" in name and f" n={n} " in name:
+        hit = name.startswith("stream_kernel_v") if kind == "v" else \
+            (f"kind={kind}>" in name and f" n={n} " in name)
+        if hit:
             return tot / cnt, KIND_BYTES[kind] * nt * 8 * n * B, name
     return None, None, None
 
@@ -337,7 +342,9 @@ def run_gpu_arm(args, w):
     # kernel time), plus the level-1 passes beside it
     times = live_kernel_times(plan, F, U, floors, cfg.eps, cfg.max_iters)
     peak, peak_kind = peak_hbm()
-    up_s, up_bytes, up_name = kernel_roofline(times, n, nt, B, 7)
+    up_s, up_bytes, up_name = kernel_roofline(times, n, nt, B, "v")
+    if up_s is None:  # configurations without the vertical fusion
+        up_s, up_bytes, up_name = kernel_roofline(times, n, nt, B, 7)
     l1 = {}
     for kind, label in ((5, "up"), (1, "down")):
         ks, kb, kn = kernel_roofline(times, n // 2, nt, B, kind)
@@ -369,9 +376,10 @@ def run_gpu_arm(args, w):
             "wall_s_to_1e-8": ms * 1e-3, "iterations": sorted(set(i for r in iters for i in r)),
             "roofline": {"bound": "hbm", "achieved": up_bytes / up_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": up_bytes / up_s / 1e9 / peak, "traffic": traffic,
-                         "kernel": "finest-level fused pass: up pass of cycle k (pre-sweeps recomputed, "
-                                   "prolong-add, nu2 sweeps) + down pass of cycle k+1 (norm leaves, nu1 "
-                                   "sweeps, residual, restriction); K_UP2DOWN, whole batch: " + up_name,
+                         "kernel": "finest-level fused pass: level-1 up pass of cycle k (in shared memory) + "
+                                   "finest up pass of cycle k (pre-sweeps recomputed, prolong-add, nu2 sweeps) + "
+                                   "finest down pass of cycle k+1 (norm leaves, nu1 sweeps, residual, "
+                                   "restriction), whole batch: " + up_name,
                          "bytes_per_launch": up_bytes, "launch_s": up_s,
                          "timing": "CUDA events on the launch stream around the plan's own launches "
                                    "(tmg_trace_enable), one solve after the timed region",
@@ -388,11 +396,12 @@ def run_gpu_arm(args, w):
             "cpu_baseline": cpu,
         }
         # whole-cycle HBM fraction over every problem-cycle of the run: this
-        # design moves 8 n_t 8 B per finest slab per V-cycle (finest fused pass
-        # 4.0 + levels >= 1 (1.5 + 2.5) / 2 / (1 - 1/2)); SURVEY 8(d)'s model
-        # (every pass stores u, separate passes) is 13 n_t 8 B
+        # design moves 7 n_t 8 B per finest slab per V-cycle (vertically fused
+        # finest pass 4.25 + level-1 down 1.5/2 + levels >= 2 (1.5 + 2.5) / 4 /
+        # (1 - 1/2)); SURVEY 8(d)'s model (separate passes, every pass stores u)
+        # is 13 n_t 8 B
         cycles = sum(sum(r) for r in iters)
-        line["cycle_hbm_frac"] = (8 * nt * 8 * n * cycles) / elapsed / 1e9 / peak
+        line["cycle_hbm_frac"] = (7 * nt * 8 * n * cycles) / elapsed / 1e9 / peak
         line["cycle_hbm_frac_survey_model"] = (13 * nt * 8 * n * cycles) / elapsed / 1e9 / peak
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -629,6 +629,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                      bool fuse_next_down = false, bool skip_up = false)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
+        const bool pr = !skip_up && pair_up(l, first_visit);
         if (l + 1 == tl) {
             TailArgs<T, NT> t = targ;
             t.f_in = fl[tl];
@@ -642,9 +643,30 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             trace_mark("tail_kernel", s);
             ++kernels_per_cycle;
         } else {
-            for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s));
+            for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s, pr));
         }
-        if (skip_up) return 0;  // level 1 under the vertical fusion: its up pass runs inside the finest pass
+        if (skip_up) return 0;  // this level's up pass runs inside the next finer level's pass
+        if (pr) {
+            // coarse pair: level l+1's up pass in shared memory feeding level l's
+            StreamArgs<T> a = level_args(l);
+            a.f = fl[l];
+            a.u_out = uA[l];
+            a.uc = uA[l + 2];
+            a.f1 = fl[l + 1];
+            a.active = d_active;
+            a.flags = SF_PROLONG | SF_WRITE_U | SF_ZERO_GUESS;
+            StreamArgs<T> a1 = a;
+            a1.n = n[l + 1];
+            const int rc = stream_v_launch<T, NT>(L[l], L[l + 1], a, a1, o.nu2, pk[l], false, s);
+            if (rc < 0) return fail(TMG_E_UNSUPPORTED, "coarse pair kernel unavailable");
+            if (rc > 0) return fail(rc, "stream_kernel_v pair: %s", cudaGetErrorString((cudaError_t)rc));
+            char what[96];
+            snprintf(what, sizeof what, "stream_kernel_v pair n=%lld+%lld", n[l], n[l + 1]);
+            CK_LAUNCH(what);
+            trace_mark(what, s);
+            ++kernels_per_cycle;
+            return 0;
+        }
         if (up2 && (!norm_up || (l == 0 && norm_up2()))) {
             // prolong-add + post-sweeps, the pre-sweeps recomputed from the
             // level's original iterate (read in place; warm-ups from the halo);
@@ -696,7 +718,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         return 0;
     }
 
-    int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s)
+    int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s,
+                      bool skip_up = false)
     {
         if (up2 && norm && !(l == 0 && norm_up2())) {
             // the up pass cannot produce the norm: take it in a separate pass
@@ -705,7 +728,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             return enqueue_norm_pass(f0, u0, s);
         }
         CKR(enqueue_down(l, f0, u0, first_visit, false, s));
-        return enqueue_rest(l, f0, u0, norm, s, first_visit);
+        return enqueue_rest(l, f0, u0, norm, s, first_visit, false, skip_up);
     }
 
     // standalone ||f - L u|| pass at the finest level (r0 / generic sizes)
@@ -732,6 +755,19 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     // Measured on config 3: 128.3 vs 131.1 ms per solve, config 2 ~1-2 %.
     bool norm_up2() const { return up2 && leaf_rows0 > 0 && SP && norm_up_env(); }
     bool norm_in() const { return leaf_rows0 > 0 && SP && !norm_up2(); }
+    // coarse pairs (level l+1's up pass inside level l's, both from the zero
+    // guess; TMG_NO_VPAIR=1 disables)
+    bool pair_up(int l, bool first_visit) const
+    {
+        static int v = -1;
+        if (v < 0) {
+            const char *e = getenv("TMG_NO_VPAIR");
+            v = (e && *e && *e != '0') ? 0 : 1;
+        }
+        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && ROWW == 64 &&
+               sizeof(T) == 8 && n[l] % 128 == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
+               aligned16(fl[l + 1]) && aligned16(uA[l]) && aligned16(uA[l + 2]);
+    }
     // vertical fusion (level-1 up pass inside the fused finest pass; TMG_NO_VFUSE=1 disables)
     bool vfuse(const void *f, const void *u) const
     {
@@ -809,7 +845,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             StreamArgs<T> a1 = a;
             a1.n = n[1];
             a1.flags = SF_PROLONG | SF_WRITE_U | SF_ZERO_GUESS;
-            const int rc = stream_v_launch<T, NT>(L[0], L[1], a, a1, o.nu2, pk[0], s);
+            const int rc = stream_v_launch<T, NT>(L[0], L[1], a, a1, o.nu2, pk[0], true, s);
             if (rc < 0) return fail(TMG_E_UNSUPPORTED, "vertical fusion unavailable");
             if (rc > 0) return fail(rc, "stream_kernel_v: %s", cudaGetErrorString((cudaError_t)rc));
             CK_LAUNCH("stream_kernel_v");

@@ -84,12 +84,12 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
 template <typename T, int NT> size_t stream_smem_bytes() { return RowLayout<T, NT, true, true>::SMEM_BYTES; }
 
 namespace {
-template <typename T, int NT, int NU, int PERM>
+template <typename T, int NT, int NU, int PERM, bool FINEST>
 int launch_v(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a, const StreamArgs<T> &a1,
              cudaStream_t s)
 {
-    auto k = stream_kernel_v<T, NT, NU, true, PERM>;
-    constexpr size_t smem = RowLayoutV<T, NT>::SMEM_BYTES;
+    auto k = stream_kernel_v<T, NT, NU, true, PERM, FINEST>;
+    constexpr size_t smem = RowLayoutV<T, NT, FINEST>::SMEM_BYTES;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -102,15 +102,15 @@ int launch_v(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<
     if (grid <= 0) return 0;
     return (int)launch_pdl(k, dim3((unsigned)grid), dim3(WARPS * 32), smem, s, L0, L1, a, a1);
 }
-template <typename T, int NT, int PERM>
+template <typename T, int NT, int PERM, bool FINEST>
 int v_by_nu(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a, const StreamArgs<T> &a1,
             int nu, cudaStream_t s)
 {
     switch (nu) {
-    case 1: return launch_v<T, NT, 1, PERM>(L0, L1, a, a1, s);
-    case 2: return launch_v<T, NT, 2, PERM>(L0, L1, a, a1, s);
-    case 3: return launch_v<T, NT, 3, PERM>(L0, L1, a, a1, s);
-    case 4: return launch_v<T, NT, 4, PERM>(L0, L1, a, a1, s);
+    case 1: return launch_v<T, NT, 1, PERM, FINEST>(L0, L1, a, a1, s);
+    case 2: return launch_v<T, NT, 2, PERM, FINEST>(L0, L1, a, a1, s);
+    case 3: return launch_v<T, NT, 3, PERM, FINEST>(L0, L1, a, a1, s);
+    case 4: return launch_v<T, NT, 4, PERM, FINEST>(L0, L1, a, a1, s);
     }
     return -2;
 }
@@ -120,15 +120,22 @@ int v_by_nu(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T
 // coupling only; -1 = not available for this (dtype, n_t): use the separate passes)
 template <typename T, int NT>
 int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
-                    const StreamArgs<T> &a1, int nu, int perm, cudaStream_t s)
+                    const StreamArgs<T> &a1, int nu, int perm, bool finest, cudaStream_t s)
 {
     if constexpr (slabs_per_lane<T, NT>() != 2 || sizeof(T) != 8) {
         return -1;
     } else {
+        if (finest) {
+            switch (perm) {
+            case P_ID: return v_by_nu<T, NT, P_ID, true>(L0, L1, a, a1, nu, s);
+            case P_ROT: return v_by_nu<T, NT, P_ROT, true>(L0, L1, a, a1, nu, s);
+            default: return v_by_nu<T, NT, P_GEN, true>(L0, L1, a, a1, nu, s);
+            }
+        }
         switch (perm) {
-        case P_ID: return v_by_nu<T, NT, P_ID>(L0, L1, a, a1, nu, s);
-        case P_ROT: return v_by_nu<T, NT, P_ROT>(L0, L1, a, a1, nu, s);
-        default: return v_by_nu<T, NT, P_GEN>(L0, L1, a, a1, nu, s);
+        case P_ID: return v_by_nu<T, NT, P_ID, false>(L0, L1, a, a1, nu, s);
+        case P_ROT: return v_by_nu<T, NT, P_ROT, false>(L0, L1, a, a1, nu, s);
+        default: return v_by_nu<T, NT, P_GEN, false>(L0, L1, a, a1, nu, s);
         }
     }
 }
@@ -174,7 +181,7 @@ template int stream_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const S
 template size_t stream_smem_bytes<TMG_T, TMG_NT>();
 template int stream_v_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const LevelC<TMG_T, TMG_NT> &,
                                             const StreamArgs<TMG_T> &, const StreamArgs<TMG_T> &, int, int,
-                                            cudaStream_t);
+                                            bool, cudaStream_t);
 template int tail_prepare<TMG_T, TMG_NT>(bool, size_t);
 template int tail_launch<TMG_T, TMG_NT>(const TailArgs<TMG_T, TMG_NT> &, bool, unsigned, size_t, cudaStream_t);
 template int coarse_serial_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, bool, const TMG_T *, TMG_T *,

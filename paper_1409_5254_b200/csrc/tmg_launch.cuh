@@ -50,7 +50,7 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
 template <typename T, int NT> size_t stream_smem_bytes();
 template <typename T, int NT>
 int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
-                    const StreamArgs<T> &a1, int nu, int perm, cudaStream_t s);
+                    const StreamArgs<T> &a1, int nu, int perm, bool finest, cudaStream_t s);
 template <typename T, int NT> int tail_prepare(bool sparse, size_t smem);
 template <typename T, int NT>
 int tail_launch(const TailArgs<T, NT> &t, bool sparse, unsigned grid, size_t smem, cudaStream_t s);
@@ -68,7 +68,7 @@ int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, in
     extern template size_t stream_smem_bytes<T, NT>();                                                  \
     extern template int stream_v_launch<T, NT>(const LevelC<T, NT> &, const LevelC<T, NT> &,             \
                                                const StreamArgs<T> &, const StreamArgs<T> &, int, int,    \
-                                               cudaStream_t);                                             \
+                                               bool, cudaStream_t);                                       \
     extern template int tail_prepare<T, NT>(bool, size_t);                                              \
     extern template int tail_launch<T, NT>(const TailArgs<T, NT> &, bool, unsigned, size_t, cudaStream_t); \
     extern template int coarse_serial_launch<T, NT>(const LevelC<T, NT> &, bool, const T *, T *, long long, \

@@ -710,30 +710,36 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
 // the next cycle's is written here and read by the level-1 down pass), like
 // the halo rows.  Warm-up: the coarse row before the chunk, then the fine row
 // before it (its u_c is that coarse row's exact second half).
-template <typename T, int NT> struct RowLayoutV {
+template <typename T, int NT, bool FINEST = true> struct RowLayoutV {
     static constexpr int W = 64;
     static constexpr int ROW = W * NT;       // elements of a 64-slab row (fine or coarse)
     static constexpr int HALF = ROW / 2;
-    static constexpr int OFF_F = 2 * ROW;    // stage: u0 rows | f0 rows | f1 row | u2 half row
-    static constexpr int OFF_F1 = 4 * ROW;
-    static constexpr int OFF_C2 = 5 * ROW;
-    static constexpr int STAGE = 5 * ROW + HALF;
-    static constexpr int ST = 2;
+    // stage: [u rows (FINEST only)] | f rows | coarse f row | coarse-coarse u half row
+    static constexpr int OFF_U = 0;
+    static constexpr int OFF_F = FINEST ? 2 * ROW : 0;
+    static constexpr int OFF_F1 = OFF_F + 2 * ROW;
+    static constexpr int OFF_C2 = OFF_F1 + ROW;
+    static constexpr int STAGE = OFF_C2 + HALF;
+    static constexpr int ST = FINEST ? 2 : 3;
     static constexpr int LB = 2;             // numpy leaves per flush (smem budget)
-    static constexpr int LEAFBUF = LB * 128;
+    static constexpr int LEAFBUF = FINEST ? LB * 128 : 0;
     static constexpr int WARPS = CtaShape<T, NT>::WARPS;
     static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + LEAFBUF);
     static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
 };
 
-template <typename T, int NT, int NU, bool SPARSE, int PERM>
+// FINEST: level 0 (K_UP2DOWN rows, in-place u, halo rows and f_1 by cycle
+// parity, norm leaves).  !FINEST: a coarse pair (levels l, l+1 >= 1, both from
+// the zero guess): K_UP2 rows at level l with u_c from the level-(l+1) row in
+// shared memory, u_l written for the next finer level's up pass.
+template <typename T, int NT, int NU, bool SPARSE, int PERM, bool FINEST = true>
 __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::MINB)
     stream_kernel_v(const __grid_constant__ LevelC<T, NT> L, const __grid_constant__ LevelC<T, NT> L1,
                     const __grid_constant__ StreamArgs<T> a, const __grid_constant__ StreamArgs<T> a1)
 {
-    using Lay = RowLayoutV<T, NT>;
-    using S = Streamer<T, NT, NU, SPARSE, K_UP2DOWN, PERM>;
+    using Lay = RowLayoutV<T, NT, FINEST>;
+    using S = Streamer<T, NT, NU, SPARSE, FINEST ? K_UP2DOWN : K_UP2, PERM>;
     using S1 = Streamer<T, NT, NU, SPARSE, K_UP2, PERM>;
     static_assert(S::P == 2, "vertical fusion needs two-slab lanes");
     constexpr int P = 2, W = 64;
@@ -757,13 +763,13 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     const int rows = (int)min((long long)a.rows_per_chunk, n / W - row0);
     const int ngroups = rows >> 1;
     const int lofs = lane * P;
-    const bool par = a.iters[(size_t)b * a.iters_stride] & 1;
+    const bool par = FINEST && (a.iters[(size_t)b * a.iters_stride] & 1);
     T *halo_in = par ? a.halo_alt : a.halo;
     T *halo_next = par ? a.halo : a.halo_alt;
-    const T *f1b = (par ? a.f1_alt : a.f1) + (size_t)b * n1 * NT;   // this cycle's f_1
-    T *fcb = (par ? (T *)a.f1 : a.f1_alt) + (size_t)b * n1 * NT;     // the next cycle's f_1
+    const T *f1b = (par ? a.f1_alt : a.f1) + (size_t)b * n1 * NT;   // this cycle's level-(l+1) f
+    T *fcb = FINEST ? (par ? (T *)a.f1 : a.f1_alt) + (size_t)b * n1 * NT : nullptr;  // next cycle's f_1
     const T *fb = a.f + (size_t)b * n * NT;
-    const T *ub = a.u_in + (size_t)b * n * NT;
+    const T *ub = FINEST ? a.u_in + (size_t)b * n * NT : nullptr;
     const T *u2b = a.uc + (size_t)b * n2 * NT;
 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * Lay::ST;
@@ -787,7 +793,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     s1.write_u = true;
     s1.vec_out = true;
     T *uo = a.u_out + ((size_t)b * n + (size_t)row0 * W + lofs) * NT;
-    T *fco = fcb + (((size_t)row0 * W + lofs) >> 1) * NT;
+    T *fco = FINEST ? fcb + (((size_t)row0 * W + lofs) >> 1) * NT : nullptr;
     uint64_t pol = 0;
     if (lane == 0) {
 #pragma unroll
@@ -800,12 +806,12 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         T *stg = ring + (size_t)(g % Lay::ST) * Lay::STAGE;
         uint64_t *bar = &bars[g % Lay::ST];
         const long long s0 = (row0 + 2LL * g) * W;      // first fine slab of the stage
-        const long long c0 = s0 >> 1;                   // first level-1 slab
+        const long long c0 = s0 >> 1;                   // first coarse slab
         const uint32_t fine = (uint32_t)(2 * Lay::ROW * sizeof(T));
         const uint32_t crow = (uint32_t)(Lay::ROW * sizeof(T));
         const uint32_t chalf = (uint32_t)(Lay::HALF * sizeof(T));
-        mbar_expect_tx(bar, 2 * fine + crow + chalf);
-        bulk_g2s(stg, ub + s0 * NT, fine, bar, pol);
+        mbar_expect_tx(bar, (FINEST ? 2 : 1) * fine + crow + chalf);
+        if (FINEST) bulk_g2s(stg + Lay::OFF_U, ub + s0 * NT, fine, bar, pol);
         bulk_g2s(stg + Lay::OFF_F, fb + s0 * NT, fine, bar, pol);
         bulk_g2s(stg + Lay::OFF_F1, f1b + c0 * NT, crow, bar, pol);
         bulk_g2s(stg + Lay::OFF_C2, u2b + (c0 >> 1) * NT, chalf, bar, pol);
@@ -813,7 +819,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     if (lane == 0)
         for (int g = 0; g < ngroups && g < Lay::ST; ++g) issue(g);
 
-    // level-1 row cr into u1row (zero original iterate)
+    // coarse row cr (zero original iterate) into u1row
     auto coarse_row = [&](long long cr, const T (&f1)[P][NT], const T (&u2)[NT]) {
         T u[P][NT];
 #pragma unroll
@@ -835,9 +841,14 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         T u[P][NT], f[P][NT], uc[NT];
 #pragma unroll
         for (int q = 0; q < P; ++q) load_slab_scalar<T, NT>(fb + (wr * W + lofs + q) * NT, f[q]);
-        load_lane<T, NT, P>(halo_in + ((size_t)b * a.chunks + chunk - 1) * Lay::ROW + lofs * NT, u);
+        if constexpr (FINEST) {
+            load_lane<T, NT, P>(halo_in + ((size_t)b * a.chunks + chunk - 1) * Lay::ROW + lofs * NT, u);
+        } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) zero_slab<T, NT>(u[q]);
+        }
         load_slab<T, NT>(u1row + Lay::HALF + (lofs >> 1) * NT, uc);
-        st.template row<true>(u, f, uc, wr * W + lofs, wr, true, b, nullptr, nullptr, false);
+        st.template row<true>(u, f, uc, wr * W + lofs, wr, true, b, nullptr, nullptr, !FINEST);
         __syncwarp();
     }
 
@@ -856,24 +867,31 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
             const long long ridx = row0 + rr;
             T u[P][NT], f[P][NT], uc[NT];
             load_lane<T, NT, P>(stg + Lay::OFF_F + qq * Lay::ROW + lofs * NT, f);
-            load_lane<T, NT, P>(stg + qq * Lay::ROW + lofs * NT, u);
+            if constexpr (FINEST) {
+                load_lane<T, NT, P>(stg + Lay::OFF_U + qq * Lay::ROW + lofs * NT, u);
+            } else {
+#pragma unroll
+                for (int q = 0; q < P; ++q) zero_slab<T, NT>(u[q]);
+            }
             load_slab<T, NT>(u1row + qq * Lay::HALF + (lofs >> 1) * NT, uc);
             if (qq == 1) {
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0 && g + Lay::ST < ngroups) issue(g + Lay::ST);
             }
-            st.halo_w = (rr == rows - 1 && chunk + 1 < a.chunks)
-                            ? halo_next + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT
-                            : nullptr;
-            if (ridx > 0) st.template row<true>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, false);
-            else st.template row<false>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, false);
+            if constexpr (FINEST)
+                st.halo_w = (rr == rows - 1 && chunk + 1 < a.chunks)
+                                ? halo_next + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT
+                                : nullptr;
+            if (ridx > 0) st.template row<true>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, !FINEST);
+            else st.template row<false>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, !FINEST);
             uo += Lay::ROW;
-            fco += Lay::HALF;
+            if constexpr (FINEST) fco += Lay::HALF;
         }
         __syncwarp();  // every lane is done with u1row before the next coarse row overwrites it
     }
-    if (st.leaf_q > 0) st.leaf_flush(b);
+    if constexpr (FINEST)
+        if (st.leaf_q > 0) st.leaf_flush(b);
 }
 
 }  // namespace tmg

@@ -626,7 +626,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     // coarse-grid correction of level l and its up pass (norm_up: the up pass
     // also produces the norm of its output -- used when the down pass cannot)
     int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s, bool first_visit = true,
-                     bool fuse_next_down = false, bool skip_up = false)
+                     bool fuse_next_down = false, bool skip_up = false, bool child_skip_down = false)
     {
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
         const bool pr = !skip_up && pair_up(l, first_visit);
@@ -643,7 +643,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             trace_mark("tail_kernel", s);
             ++kernels_per_cycle;
         } else {
-            for (int g = 0; g < o.gamma; ++g) CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s, pr));
+            for (int g = 0; g < o.gamma; ++g)
+                CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s, pr, child_skip_down && g == 0));
         }
         if (skip_up) return 0;  // this level's up pass runs inside the next finer level's pass
         if (pr) {
@@ -719,7 +720,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     }
 
     int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s,
-                      bool skip_up = false)
+                      bool skip_up = false, bool skip_down = false)
     {
         if (up2 && norm && !(l == 0 && norm_up2())) {
             // the up pass cannot produce the norm: take it in a separate pass
@@ -727,8 +728,13 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             CKR(enqueue_rest(l, f0, u0, false, s, first_visit));
             return enqueue_norm_pass(f0, u0, s);
         }
-        CKR(enqueue_down(l, f0, u0, first_visit, false, s));
-        return enqueue_rest(l, f0, u0, norm, s, first_visit, false, skip_up);
+        bool dp = false;
+        if (!skip_down) {
+            dp = pair_down(l, first_visit);
+            if (dp) CKR(enqueue_down_pair(l, s, false));  // levels l and l+1
+            else CKR(enqueue_down(l, f0, u0, first_visit, false, s));
+        }
+        return enqueue_rest(l, f0, u0, norm, s, first_visit, false, skip_up, dp);
     }
 
     // standalone ||f - L u|| pass at the finest level (r0 / generic sizes)
@@ -767,6 +773,44 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && ROWW == 64 &&
                sizeof(T) == 8 && n[l] % 128 == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
                aligned16(fl[l + 1]) && aligned16(uA[l]) && aligned16(uA[l + 2]);
+    }
+    // coarse down pairs (level l's down pass feeding level l+1's through shared
+    // memory, both from the zero guess; TMG_NO_DPAIR=1 disables)
+    bool pair_down(int l, bool first_visit) const
+    {
+        static int v = -1;
+        if (v < 0) {
+            const char *e = getenv("TMG_NO_DPAIR");
+            v = (e && *e && *e != '0') ? 0 : 1;
+        }
+        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && ROWW == 64 &&
+               sizeof(T) == 8 && n[l] % 128 == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
+               aligned16(fl[l + 1]) && aligned16(fl[l + 2]) && (l != 1 || !fl1_alt || aligned16(fl1_alt));
+    }
+    int enqueue_down_pair(int l, cudaStream_t s, bool f_by_parity)
+    {
+        StreamArgs<T> a = level_args(l);
+        a.f = fl[l];
+        if (f_by_parity) {
+            a.f_alt = fl1_alt;
+            a.iters = &d_st[0].iters;
+            a.iters_stride = (int)(sizeof(ProbState) / sizeof(int));
+        }
+        a.fc = fl[l + 1];
+        a.active = d_active;
+        a.flags = SF_RESTRICT | SF_ZERO_GUESS;
+        StreamArgs<T> a1 = a;
+        a1.n = n[l + 1];
+        a1.fc = fl[l + 2];
+        const int rc = stream_d_launch<T, NT>(L[l], L[l + 1], a, a1, o.nu1, pk[l], s);
+        if (rc < 0) return fail(TMG_E_UNSUPPORTED, "coarse down pair unavailable");
+        if (rc > 0) return fail(rc, "stream_kernel_d: %s", cudaGetErrorString((cudaError_t)rc));
+        char what[96];
+        snprintf(what, sizeof what, "stream_kernel_d pair n=%lld+%lld", n[l], n[l + 1]);
+        CK_LAUNCH(what);
+        trace_mark(what, s);
+        ++kernels_per_cycle;
+        return 0;
     }
     // vertical fusion (level-1 up pass inside the fused finest pass; TMG_NO_VFUSE=1 disables)
     bool vfuse(const void *f, const void *u) const
@@ -826,8 +870,10 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             // vertical fusion: level 1's down pass (f_1 by parity), the coarser
             // levels, then ONE finest pass = level-1 up pass + finest up pass +
             // the next cycle's finest down pass
-            CKR(enqueue_down(1, f, u, true, false, s, true));
-            CKR(enqueue_rest(1, f, u, false, s, true, false, true));
+            const bool dp1 = pair_down(1, true);
+            if (dp1) CKR(enqueue_down_pair(1, s, true));
+            else CKR(enqueue_down(1, f, u, true, false, s, true));
+            CKR(enqueue_rest(1, f, u, false, s, true, false, true, dp1));
             StreamArgs<T> a = level_args(0);
             a.f = (const T *)f;
             a.u_in = (const T *)u;

@@ -116,6 +116,55 @@ int v_by_nu(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T
 }
 }  // namespace
 
+namespace {
+template <typename T, int NT, int NU, int PERM>
+int launch_d(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a, const StreamArgs<T> &a1,
+             cudaStream_t s)
+{
+    auto k = stream_kernel_d<T, NT, NU, true, PERM>;
+    constexpr size_t smem = RowLayoutD<T, NT>::SMEM_BYTES;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+    }
+    const long long warps = (long long)a.batch * a.chunks;
+    constexpr int WARPS = CtaShape<T, NT>::WARPS;
+    const long long grid = (warps + WARPS - 1) / WARPS;
+    if (grid <= 0) return 0;
+    return (int)launch_pdl(k, dim3((unsigned)grid), dim3(WARPS * 32), smem, s, L0, L1, a, a1);
+}
+template <typename T, int NT, int PERM>
+int d_by_nu(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a, const StreamArgs<T> &a1,
+            int nu, cudaStream_t s)
+{
+    switch (nu) {
+    case 1: return launch_d<T, NT, 1, PERM>(L0, L1, a, a1, s);
+    case 2: return launch_d<T, NT, 2, PERM>(L0, L1, a, a1, s);
+    case 3: return launch_d<T, NT, 3, PERM>(L0, L1, a, a1, s);
+    case 4: return launch_d<T, NT, 4, PERM>(L0, L1, a, a1, s);
+    }
+    return -2;
+}
+}  // namespace
+
+// coarse down-pass pairs (two-slab lanes, fp64, sparse coupling; -1 = not available)
+template <typename T, int NT>
+int stream_d_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
+                    const StreamArgs<T> &a1, int nu, int perm, cudaStream_t s)
+{
+    if constexpr (slabs_per_lane<T, NT>() != 2 || sizeof(T) != 8) {
+        return -1;
+    } else {
+        switch (perm) {
+        case P_ID: return d_by_nu<T, NT, P_ID>(L0, L1, a, a1, nu, s);
+        case P_ROT: return d_by_nu<T, NT, P_ROT>(L0, L1, a, a1, nu, s);
+        default: return d_by_nu<T, NT, P_GEN>(L0, L1, a, a1, nu, s);
+        }
+    }
+}
+
 // the finest pass with the level-1 up pass fused in (two-slab lanes, sparse
 // coupling only; -1 = not available for this (dtype, n_t): use the separate passes)
 template <typename T, int NT>
@@ -179,6 +228,9 @@ template int coarse_scan_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, co
 template int stream_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
                                           int, bool, cudaStream_t);
 template size_t stream_smem_bytes<TMG_T, TMG_NT>();
+template int stream_d_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const LevelC<TMG_T, TMG_NT> &,
+                                            const StreamArgs<TMG_T> &, const StreamArgs<TMG_T> &, int, int,
+                                            cudaStream_t);
 template int stream_v_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const LevelC<TMG_T, TMG_NT> &,
                                             const StreamArgs<TMG_T> &, const StreamArgs<TMG_T> &, int, int,
                                             bool, cudaStream_t);

@@ -49,6 +49,9 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
                   cudaStream_t s);
 template <typename T, int NT> size_t stream_smem_bytes();
 template <typename T, int NT>
+int stream_d_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
+                    const StreamArgs<T> &a1, int nu, int perm, cudaStream_t s);
+template <typename T, int NT>
 int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
                     const StreamArgs<T> &a1, int nu, int perm, bool finest, cudaStream_t s);
 template <typename T, int NT> int tail_prepare(bool sparse, size_t smem);
@@ -66,6 +69,9 @@ int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, in
     extern template int stream_launch<T, NT>(const LevelC<T, NT> &, const StreamArgs<T> &, int, int, int, \
                                              bool, cudaStream_t);                                       \
     extern template size_t stream_smem_bytes<T, NT>();                                                  \
+    extern template int stream_d_launch<T, NT>(const LevelC<T, NT> &, const LevelC<T, NT> &,             \
+                                               const StreamArgs<T> &, const StreamArgs<T> &, int, int,    \
+                                               cudaStream_t);                                             \
     extern template int stream_v_launch<T, NT>(const LevelC<T, NT> &, const LevelC<T, NT> &,             \
                                                const StreamArgs<T> &, const StreamArgs<T> &, int, int,    \
                                                bool, cudaStream_t);                                       \

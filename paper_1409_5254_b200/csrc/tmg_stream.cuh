@@ -894,4 +894,148 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         if (st.leaf_q > 0) st.leaf_flush(b);
 }
 
+
+// ---------------------------------------------------------------------------
+// Coarse down-pass pairs (two-slab lanes, both levels from the zero guess):
+// per ring stage the two level-l rows' down passes (nu1 sweeps, residual,
+// restriction) leave their restricted rows in a per-warp shared-memory row,
+// which is stored as f_{l+1} and at once swept as one level-(l+1) row (its own
+// down pass: f_{l+2}) -- one launch instead of two, f_{l+1} not re-read.
+// Warm-up: three level-l rows before the chunk (the first for the carries,
+// the next two for the level-(l+1) row before the chunk), then that row.
+template <typename T, int NT> struct RowLayoutD {
+    static constexpr int W = 64;
+    static constexpr int ROW = W * NT;
+    static constexpr int HALF = ROW / 2;
+    static constexpr int STAGE = 2 * ROW;    // two level-l f rows
+    static constexpr int ST = 3;
+    static constexpr int WARPS = CtaShape<T, NT>::WARPS;
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW);
+    static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
+    static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
+};
+
+template <typename T, int NT, int NU, bool SPARSE, int PERM>
+__global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::MINB)
+    stream_kernel_d(const __grid_constant__ LevelC<T, NT> L, const __grid_constant__ LevelC<T, NT> L1,
+                    const __grid_constant__ StreamArgs<T> a, const __grid_constant__ StreamArgs<T> a1)
+{
+    using Lay = RowLayoutD<T, NT>;
+    using S = Streamer<T, NT, NU, SPARSE, K_DOWN, PERM>;
+    static_assert(S::P == 2, "down pairs need two-slab lanes");
+    constexpr int P = 2, W = 64;
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const long long gw = (long long)blockIdx.x * Lay::WARPS + warp;
+    if (gw >= (long long)a.batch * a.chunks) return;
+    const int b = (int)(gw / a.chunks);
+    const long long chunk = gw - (long long)b * a.chunks;
+    if (a.active && !a.active[b]) return;
+
+    const long long n = a.n, n1 = n >> 1, n2 = n >> 2;
+    S st{L, a, lane, a.flags};
+    st.nc = n1;
+    S s1{L1, a1, lane, a1.flags};
+    s1.nc = n2;
+    const long long row0 = chunk * a.rows_per_chunk;          // even; every row full (n % 128 == 0)
+    const int rows = (int)min((long long)a.rows_per_chunk, n / W - row0);
+    const int ngroups = rows >> 1;
+    const int lofs = lane * P;
+    const T *fsrc = (a.f_alt && (a.iters[(size_t)b * a.iters_stride] & 1)) ? a.f_alt : a.f;
+    const T *fb = fsrc + (size_t)b * n * NT;
+    T *f1b = a.fc + (size_t)b * n1 * NT;     // f_{l+1} (stored)
+    T *f2b = a1.fc + (size_t)b * n2 * NT;    // f_{l+2}
+
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * Lay::ST;
+    unsigned char *wbase = smem + Lay::BAR_BYTES + (size_t)warp * Lay::BYTES_PER_WARP;
+    T *c1row = reinterpret_cast<T *>(wbase);
+    T *ring = c1row + Lay::ROW;
+#pragma unroll
+    for (int k = 0; k <= NU; ++k) {
+        cpl_zero(st.carry[k]);
+        cpl_zero(s1.carry[k]);
+    }
+    st.leaf_q = s1.leaf_q = 0;
+    st.leaf0 = s1.leaf0 = 0;
+    st.halo_w = s1.halo_w = nullptr;
+    st.write_u = s1.write_u = false;
+    st.vec_out = s1.vec_out = false;
+    uint64_t pol = 0;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < Lay::ST; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        pol = policy_evict_first();
+    }
+    __syncwarp();
+    auto issue = [&](int g) {  // lane 0 only
+        T *stg = ring + (size_t)(g % Lay::ST) * Lay::STAGE;
+        uint64_t *bar = &bars[g % Lay::ST];
+        const long long s0 = (row0 + 2LL * g) * W;
+        const uint32_t bytes = (uint32_t)(Lay::STAGE * sizeof(T));
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(stg, fb + s0 * NT, bytes, bar, pol);
+    };
+    if (lane == 0)
+        for (int g = 0; g < ngroups && g < Lay::ST; ++g) issue(g);
+
+    // one level-l row from f (zero guess); its restricted row half -> c1row
+    auto fine_row = [&](long long r, const T (&f)[P][NT], int half, bool warm) {
+        T u[P][NT], uc[NT];
+#pragma unroll
+        for (int q = 0; q < P; ++q) zero_slab<T, NT>(u[q]);
+        zero_slab<T, NT>(uc);
+        T *dst = warm ? nullptr : c1row + half * Lay::HALF + (lofs >> 1) * NT;
+        if (r > 0) st.template row<true>(u, f, uc, r * W + lofs, r, warm, b, nullptr, dst, true);
+        else st.template row<false>(u, f, uc, r * W + lofs, r, warm, b, nullptr, dst, true);
+    };
+    // the level-(l+1) row cr from c1row: store it as f_{l+1} (unless a warm-up
+    // row of the previous chunk), then its own down pass -> f_{l+2}
+    auto coarse_row = [&](long long cr, bool store) {
+        __syncwarp();
+        T f[P][NT], u[P][NT], uc[NT];
+        load_lane<T, NT, P>(c1row + lofs * NT, f);
+        if (store) store_lane<T, NT, P>(f1b + (cr * W + lofs) * NT, f);
+#pragma unroll
+        for (int q = 0; q < P; ++q) zero_slab<T, NT>(u[q]);
+        zero_slab<T, NT>(uc);
+        T *fco2 = store ? f2b + ((cr * W + lofs) >> 1) * NT : nullptr;
+        if (cr > 0) s1.template row<true>(u, f, uc, cr * W + lofs, cr, !store, b, nullptr, fco2, true);
+        else s1.template row<false>(u, f, uc, cr * W + lofs, cr, !store, b, nullptr, fco2, true);
+        __syncwarp();
+    };
+
+    if (row0 > 0) {
+        // warm-up: level-l rows row0-3 (carries only), row0-2 and row0-1 (the
+        // level-(l+1) row before the chunk), then that row (carries only)
+        for (long long r = max(0LL, row0 - 3); r < row0; ++r) {
+            T f[P][NT];
+#pragma unroll
+            for (int q = 0; q < P; ++q) load_slab_scalar<T, NT>(fb + (r * W + lofs + q) * NT, f[q]);
+            fine_row(r, f, (int)(r & 1), r == row0 - 3);
+        }
+        coarse_row((row0 >> 1) - 1, false);
+    }
+
+    for (int g = 0; g < ngroups; ++g) {
+        const T *stg = ring + (size_t)(g % Lay::ST) * Lay::STAGE;
+        mbar_wait(&bars[g % Lay::ST], (uint32_t)((g / Lay::ST) & 1));
+#pragma unroll 1
+        for (int qq = 0; qq < 2; ++qq) {
+            T f[P][NT];
+            load_lane<T, NT, P>(stg + qq * Lay::ROW + lofs * NT, f);
+            if (qq == 1) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0 && g + Lay::ST < ngroups) issue(g + Lay::ST);
+            }
+            fine_row(row0 + 2 * g + qq, f, qq, false);
+        }
+        coarse_row((row0 >> 1) + g, true);
+    }
+}
+
 }  // namespace tmg

@@ -248,7 +248,7 @@ def kernel_roofline(times, n, nt, B, kind):
     the stream kernel of a kind at the level with n slabs per problem (kind
     "v": the vertically fused finest pass)."""
     for name, (cnt, tot) in times.items():
-        hit = name.startswith("stream_kernel_v") if kind == "v" else \
+        hit = name.startswith("stream_kernel_v (") if kind == "v" else \
             (f"kind={kind}>" in name and f" n={n} " in name)
         if hit:
             return tot / cnt, KIND_BYTES[kind] * nt * 8 * n * B, name
@@ -346,11 +346,15 @@ def run_gpu_arm(args, w):
     if up_s is None:  # configurations without the vertical fusion
         up_s, up_bytes, up_name = kernel_roofline(times, n, nt, B, 7)
     l1 = {}
-    for kind, label in ((5, "up"), (1, "down")):
-        ks, kb, kn = kernel_roofline(times, n // 2, nt, B, kind)
-        if ks:
-            l1[label] = {"kernel": kn, "bytes_per_launch": kb, "launch_s": ks, "achieved": kb / ks / 1e9,
-                         "frac": kb / ks / 1e9 / peak}
+    # the largest coarse pair kernels: down pair (levels 1, 2; 1.75 n_t 8 B per
+    # level-1 slab) and up pair (levels 2, 3; 2.75 n_t 8 B per level-2 slab)
+    for label, prefix, nl, per in (("down_pair_1_2", "stream_kernel_d pair n=%d+" % (n // 2), n // 2, 1.75),
+                                   ("up_pair_2_3", "stream_kernel_v pair n=%d+" % (n // 4), n // 4, 2.75)):
+        for name, (cnt, tot) in times.items():
+            if name.startswith(prefix):
+                kb = per * nt * 8 * nl * B
+                l1[label] = {"kernel": name, "bytes_per_launch": kb, "launch_s": tot / cnt,
+                             "achieved": kb / (tot / cnt) / 1e9, "frac": kb / (tot / cnt) / 1e9 / peak}
     traffic = None
     try:
         with open(PROFILE_SUMMARY) as fh:
@@ -385,7 +389,7 @@ def run_gpu_arm(args, w):
                                    "(tmg_trace_enable), one solve after the timed region",
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "frac_of_nominal_8TBs": up_bytes / up_s / 1e9 / 8000.0,
-                         "level1_passes": l1},
+                         "coarse_pairs": l1},
             "e2e": {"value": dof_e2e / e2e_time, "unit": UNIT,
                     "h2d_bytes_per_step": B * n * nt * 8, "d2h_bytes_per_step": B * n * nt * 8,
                     "steps": e2e_steps, "path": "DevicePlan.solve_host -> C ABI tmg_plan_solve_host with pinned "

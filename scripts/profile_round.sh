@@ -3,8 +3,9 @@
 #   1. bench.py (the JSON line, CPU baseline included)
 #   2. ncu launch list of bench.py (gpu__time_duration per launch, serialised)
 #   3. ncu --set full of the two dominant kernels of one solve (the finest
-#      level's vertically fused pass, stream_kernel_v; the level-1 down pass,
-#      K_DOWN), located from a launch list of scripts/ncu_target.py
+#      level's vertically fused pass, stream_kernel_v<..., FINEST>; the largest
+#      coarse down pair, stream_kernel_d), located from a launch list of
+#      scripts/ncu_target.py
 # Usage (from the repo root, under gpurun):  bash scripts/profile_round.sh [tag]
 set -u
 TAG=${1:-r01}
@@ -29,14 +30,14 @@ norm = lambda k: k.replace("(int)", "").replace("(bool)", "").replace("true", "1
 def best(tag):
     seq = [float(r[vi].replace(",", "")) for r in rows if tag in norm(r[ki])]
     return max(range(len(seq)), key=lambda i: seq[i]) if seq else 0
-print(best("stream_kernel_v<double, 2, 1, 1,"), best("stream_kernel<double, 2, 1, 1, 1,"))
+print(best("stream_kernel_v<double, 2, 1, 1, 2, 1>"), best("stream_kernel_d<double, 2, 1, 1,"))
 EOF
 )
 echo "skip kind4=$SKIP4 kind5=$SKIP5"
-for K in v 1; do
+for K in v d; do
     S=$([ $K = v ] && echo $SKIP4 || echo $SKIP5)
-    if [ $K = v ]; then RX="regex:stream_kernel_v<"; else
-        RX="regex:stream_kernel<double, (\\(int\\))?2, (\\(int\\))?1, (\\(bool\\))?(1|true), (\\(int\\))?$K,"; fi
+    if [ $K = v ]; then RX="regex:stream_kernel_v<double, (\\(int\\))?2, (\\(int\\))?1, (\\(bool\\))?(1|true), (\\(int\\))?2, (\\(bool\\))?(1|true)>";
+    else RX="regex:stream_kernel_d<"; fi
     timeout 900 ncu --set full --import-source on --clock-control none \
         --kernel-name-base demangled \
         -k "$RX" --launch-skip $S --launch-count 1 \

@@ -394,7 +394,7 @@ def run_gpu_arm(args, w):
                     "h2d_bytes_per_step": B * n * nt * 8, "d2h_bytes_per_step": B * n * nt * 8,
                     "steps": e2e_steps, "path": "DevicePlan.solve_host -> C ABI tmg_plan_solve_host with pinned "
                     "host buffers: H2D f, solve (zero guess), D2H u; 16 pipelined sub-batches "
-                    "(copy-in / copy-out streams, two compute streams) overlap copies with solves"},
+                    "(copy-in / copy-out streams, three compute streams) overlap copies with solves"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -424,7 +424,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         cudaFree(d_fh);
         cudaFree(d_uh);
         if (ev_h2d) cudaEventDestroy(ev_h2d);
-        for (cudaStream_t st : {cs_in, cs_out, cs_cmp[0], cs_cmp[1]})
+        for (cudaStream_t st : {cs_in, cs_out, cs_cmp[0], cs_cmp[1], cs_cmp[2], cs_cmp[3]})
             if (st) cudaStreamDestroy(st);
         cudaFree(gstore);
         cudaFree(leaves);
@@ -1019,7 +1019,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     T *d_fh = nullptr, *d_uh = nullptr;  // device copies for the host-buffer entry point
     cudaEvent_t ev_h2d = nullptr;         // this sub-batch's inputs are on the device
-    cudaStream_t cs_in = nullptr, cs_out = nullptr, cs_cmp[2] = {nullptr, nullptr};  // host-buffer pipeline
+    cudaStream_t cs_in = nullptr, cs_out = nullptr, cs_cmp[4] = {};  // host-buffer pipeline
     std::vector<tmg_level_desc> descs;   // kept to build sub-batch plans
     std::vector<std::unique_ptr<Plan>> subs;
 
@@ -1069,9 +1069,9 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                    int max_iters) override
     {
         // Pipelined sub-batches: copy-in and copy-out on their own streams, the
-        // solves alternating between two compute streams (so one sub-batch's
+        // solves rotating over three compute streams (so one sub-batch's
         // latency-bound coarse levels overlap another's bandwidth-bound fine
-        // levels), 4 sub-plans in rotation; the PCIe traffic of every sub-batch
+        // levels), 6 sub-plans in rotation; the PCIe traffic of every sub-batch
         // but the first and last hides under the solves.
         // sub-batch count measured on config 3 (B = 64): 4 -> 163 ms, 8 -> 149 ms,
         // 16 -> 145 ms, 32 -> 168 ms per host-buffer solve
@@ -1086,8 +1086,13 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             return collect();
         }
         const long long bc = B / nch;
-        const int nsub = std::min(nch, 4);
-        if ((int)subs.size() != nsub) {
+        static int ncs = -1;  // compute streams (TMG_HOST_STREAMS, 1..4)
+        if (ncs < 0) {
+            const char *e = getenv("TMG_HOST_STREAMS");
+            ncs = e ? std::min(4, std::max(1, atoi(e))) : 3;  // measured: 1 -> 156, 2 -> 122.5, 3 -> 118, 4 -> 119 ms
+        }
+        const int nsub = std::min(nch, 2 * ncs);
+        if ((int)subs.size() != nsub || subs[0]->B != bc) {
             subs.clear();
             for (int k = 0; k < nsub; ++k) {
                 auto p = std::make_unique<Plan>();
@@ -1098,8 +1103,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         if (!cs_in) {
             CK(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
             CK(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
-            CK(cudaStreamCreateWithFlags(&cs_cmp[0], cudaStreamNonBlocking));
-            CK(cudaStreamCreateWithFlags(&cs_cmp[1], cudaStreamNonBlocking));
+            for (int k = 0; k < 4; ++k) CK(cudaStreamCreateWithFlags(&cs_cmp[k], cudaStreamNonBlocking));
         }
         const size_t per = (size_t)n[0] * NT * bc;
         last_max_iters = max_iters;
@@ -1124,7 +1128,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             Plan &p = *subs[c % nsub];
             CKR(p.enqueue_host_async((const T *)f + c * per, u0 ? (const T *)u0 + c * per : nullptr,
                                      (T *)u_out + c * per, floor_ + c * bc, eps, max_iters, cs_in,
-                                     cs_cmp[c % 2], cs_out));
+                                     cs_cmp[c % ncs], cs_out));
         }
         for (int c = std::max(0, nch - nsub); c < nch; ++c) CKR(gather(c));
         return 0;

@@ -461,3 +461,29 @@ def test_solve_bitwise_repeatable():
         else:
             assert torch.equal(out[0], ref[0])
             assert out[1] == ref[1]
+
+
+# the fused finest pass (level-1 up + finest up + next finest down), the coarse
+# up/down pairs and their warm-up rows, for every sweep count and a batch
+@pytest.mark.parametrize("p_t,n,nu,B", [(1, 1 << 15, 2, 1), (1, 1 << 15, 3, 2), (0, 1 << 16, 4, 1),
+                                        (1, 3 << 13, 1, 2)])
+def test_fused_passes_vs_oracle(oracle_mod, p_t, n, nu, B):
+    T = 1.0
+    basis = tmg.BasisSpec(p_t)
+    hier = tmg.TimeHierarchy.build(basis, T / n, n, coarsest=2)
+    cfg = tmg.CycleConfig(nu1=nu, nu2=nu, eps=1e-9)
+    F = []
+    for b in range(B):
+        a, phi, u0 = problems.forcing_params(11 + b)
+        F.append(tmg.rhs_moments(problems.make_forcing(a, phi, T), basis, T / n, n, u0=u0))
+    F = np.stack(F)
+    import torch
+    floors = [1e-12 * float(np.linalg.norm(F[b])) for b in range(B)]
+    U, stats = tmg.solve_batched(hier, torch.from_numpy(F).cuda(), None, cfg, floors=floors)
+    U = U.cpu().numpy()
+    for b in range(B):
+        ur, norms, iters = oracle_mod.iterate(hier, omegas(hier), F[b], np.zeros_like(F[b]), nu, nu,
+                                              1e-9, 250)
+        assert stats[b].iterations == iters
+        assert stats[b].residual_norms == norms
+        assert same_bits(U[b], ur)

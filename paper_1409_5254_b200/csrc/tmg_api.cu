@@ -761,6 +761,17 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     // Measured on config 3: 128.3 vs 131.1 ms per solve, config 2 ~1-2 %.
     bool norm_up2() const { return up2 && leaf_rows0 > 0 && SP && norm_up_env(); }
     bool norm_in() const { return leaf_rows0 > 0 && SP && !norm_up2(); }
+    // pairs with one-slab lanes (n_t >= 3 fp64): TMG_PAIR_P1=0 disables
+    static bool pair_rows_ok()
+    {
+        if (ROWW == 64) return true;
+        static int v = -1;
+        if (v < 0) {
+            const char *e = getenv("TMG_PAIR_P1");
+            v = (e && *e == '0') ? 0 : 1;
+        }
+        return v == 1;
+    }
     // coarse pairs (level l+1's up pass inside level l's, both from the zero
     // guess; TMG_NO_VPAIR=1 disables)
     bool pair_up(int l, bool first_visit) const
@@ -770,8 +781,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             const char *e = getenv("TMG_NO_VPAIR");
             v = (e && *e && *e != '0') ? 0 : 1;
         }
-        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && ROWW == 64 &&
-               sizeof(T) == 8 && n[l] % 128 == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
+        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
+               sizeof(T) == 8 && n[l] % (2 * ROWW) == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
                aligned16(fl[l + 1]) && aligned16(uA[l]) && aligned16(uA[l + 2]);
     }
     // coarse down pairs (level l's down pass feeding level l+1's through shared
@@ -783,8 +794,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             const char *e = getenv("TMG_NO_DPAIR");
             v = (e && *e && *e != '0') ? 0 : 1;
         }
-        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && ROWW == 64 &&
-               sizeof(T) == 8 && n[l] % 128 == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
+        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
+               sizeof(T) == 8 && n[l] % (2 * ROWW) == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
                aligned16(fl[l + 1]) && aligned16(fl[l + 2]) && (l != 1 || !fl1_alt || aligned16(fl1_alt));
     }
     int enqueue_down_pair(int l, cudaStream_t s, bool f_by_parity)

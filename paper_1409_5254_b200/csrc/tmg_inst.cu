@@ -154,7 +154,7 @@ template <typename T, int NT>
 int stream_d_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
                     const StreamArgs<T> &a1, int nu, int perm, cudaStream_t s)
 {
-    if constexpr (slabs_per_lane<T, NT>() != 2 || sizeof(T) != 8) {
+    if constexpr (sizeof(T) != 8) {
         return -1;
     } else {
         switch (perm) {
@@ -171,14 +171,18 @@ template <typename T, int NT>
 int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
                     const StreamArgs<T> &a1, int nu, int perm, bool finest, cudaStream_t s)
 {
-    if constexpr (slabs_per_lane<T, NT>() != 2 || sizeof(T) != 8) {
+    if constexpr (sizeof(T) != 8) {
         return -1;
     } else {
         if (finest) {
-            switch (perm) {
-            case P_ID: return v_by_nu<T, NT, P_ID, true>(L0, L1, a, a1, nu, s);
-            case P_ROT: return v_by_nu<T, NT, P_ROT, true>(L0, L1, a, a1, nu, s);
-            default: return v_by_nu<T, NT, P_GEN, true>(L0, L1, a, a1, nu, s);
+            if constexpr (slabs_per_lane<T, NT>() != 2) return -1;
+            else
+            {
+                switch (perm) {
+                case P_ID: return v_by_nu<T, NT, P_ID, true>(L0, L1, a, a1, nu, s);
+                case P_ROT: return v_by_nu<T, NT, P_ROT, true>(L0, L1, a, a1, nu, s);
+                default: return v_by_nu<T, NT, P_GEN, true>(L0, L1, a, a1, nu, s);
+                }
             }
         }
         switch (perm) {

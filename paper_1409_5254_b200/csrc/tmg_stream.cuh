@@ -711,7 +711,8 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
 // the halo rows.  Warm-up: the coarse row before the chunk, then the fine row
 // before it (its u_c is that coarse row's exact second half).
 template <typename T, int NT, bool FINEST = true> struct RowLayoutV {
-    static constexpr int W = 64;
+    static constexpr int P = slabs_per_lane<T, NT>();
+    static constexpr int W = 32 * P;
     static constexpr int ROW = W * NT;       // elements of a 64-slab row (fine or coarse)
     static constexpr int HALF = ROW / 2;
     // stage: [u rows (FINEST only)] | f rows | coarse f row | coarse-coarse u half row
@@ -723,8 +724,10 @@ template <typename T, int NT, bool FINEST = true> struct RowLayoutV {
     static constexpr int ST = FINEST ? 2 : 3;
     static constexpr int LB = 2;             // numpy leaves per flush (smem budget)
     static constexpr int LEAFBUF = FINEST ? LB * 128 : 0;
+    static constexpr int RSTRIDE = NT * NT + 2;
+    static constexpr int RELEMS = P == 1 ? 2 * (2 * RSTRIDE) : 0;  // both levels' (R1, R2), one-slab lanes
     static constexpr int WARPS = CtaShape<T, NT>::WARPS;
-    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + LEAFBUF);
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + LEAFBUF + RELEMS);
     static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
 };
@@ -741,8 +744,8 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     using Lay = RowLayoutV<T, NT, FINEST>;
     using S = Streamer<T, NT, NU, SPARSE, FINEST ? K_UP2DOWN : K_UP2, PERM>;
     using S1 = Streamer<T, NT, NU, SPARSE, K_UP2, PERM>;
-    static_assert(S::P == 2, "vertical fusion needs two-slab lanes");
-    constexpr int P = 2, W = 64;
+    static_assert(S::P == 2 || !FINEST, "the fused finest pass needs two-slab lanes");
+    constexpr int P = S::P, W = 32 * P;
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_trigger();
     pdl_wait();
@@ -778,6 +781,18 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     st.lb = Lay::LB;
     T *u1row = reinterpret_cast<T *>(wbase) + Lay::LEAFBUF;
     T *ring = u1row + Lay::ROW;
+    if constexpr (P == 1) {
+        T *rs = ring + Lay::STAGE * Lay::ST;
+        for (int i = lane; i < NT * NT; i += 32) {
+            rs[i] = L.R1[i];
+            rs[Lay::RSTRIDE + i] = L.R2[i];
+            rs[2 * Lay::RSTRIDE + i] = L1.R1[i];
+            rs[3 * Lay::RSTRIDE + i] = L1.R2[i];
+        }
+        __syncwarp();
+        st.Rs = rs + ((lane & 1) ? Lay::RSTRIDE : 0);
+        s1.Rs = rs + 2 * Lay::RSTRIDE + ((lane & 1) ? Lay::RSTRIDE : 0);
+    }
 #pragma unroll
     for (int k = 0; k <= S::NPRE + NU + S::NPOST; ++k) cpl_zero(st.carry[k]);
 #pragma unroll
@@ -904,13 +919,17 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
 // Warm-up: three level-l rows before the chunk (the first for the carries,
 // the next two for the level-(l+1) row before the chunk), then that row.
 template <typename T, int NT> struct RowLayoutD {
-    static constexpr int W = 64;
+    static constexpr int P = slabs_per_lane<T, NT>();
+    static constexpr int W = 32 * P;
     static constexpr int ROW = W * NT;
     static constexpr int HALF = ROW / 2;
     static constexpr int STAGE = 2 * ROW;    // two level-l f rows
     static constexpr int ST = 3;
+    // one-slab lanes keep both levels' transfer blocks in shared memory
+    static constexpr int RSTRIDE = NT * NT + 2;
+    static constexpr int RELEMS = P == 1 ? 2 * (2 * RSTRIDE) : 0;
     static constexpr int WARPS = CtaShape<T, NT>::WARPS;
-    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW);
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + RELEMS);
     static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
 };
@@ -922,8 +941,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
 {
     using Lay = RowLayoutD<T, NT>;
     using S = Streamer<T, NT, NU, SPARSE, K_DOWN, PERM>;
-    static_assert(S::P == 2, "down pairs need two-slab lanes");
-    constexpr int P = 2, W = 64;
+    constexpr int P = S::P, W = 32 * P;
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_trigger();
     pdl_wait();
@@ -953,6 +971,19 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     unsigned char *wbase = smem + Lay::BAR_BYTES + (size_t)warp * Lay::BYTES_PER_WARP;
     T *c1row = reinterpret_cast<T *>(wbase);
     T *ring = c1row + Lay::ROW;
+    if constexpr (P == 1) {
+        // per-warp copies of both levels' (R1, R2); odd lanes use R2
+        T *rs = ring + Lay::STAGE * Lay::ST;
+        for (int i = lane; i < NT * NT; i += 32) {
+            rs[i] = L.R1[i];
+            rs[Lay::RSTRIDE + i] = L.R2[i];
+            rs[2 * Lay::RSTRIDE + i] = L1.R1[i];
+            rs[3 * Lay::RSTRIDE + i] = L1.R2[i];
+        }
+        __syncwarp();
+        st.Rs = rs + ((lane & 1) ? Lay::RSTRIDE : 0);
+        s1.Rs = rs + 2 * Lay::RSTRIDE + ((lane & 1) ? Lay::RSTRIDE : 0);
+    }
 #pragma unroll
     for (int k = 0; k <= NU; ++k) {
         cpl_zero(st.carry[k]);

@@ -487,3 +487,28 @@ def test_fused_passes_vs_oracle(oracle_mod, p_t, n, nu, B):
         assert stats[b].iterations == iters
         assert stats[b].residual_norms == norms
         assert same_bits(U[b], ur)
+
+
+# fp32 plans (the throughput variant: FMA + precomputed damped inverse) through
+# the same fused passes: converge to the fp64 solution within fp32 accuracy
+@pytest.mark.parametrize("p_t", [1, 2])
+def test_fp32_plan_solve_close_to_fp64(p_t):
+    import torch
+    n = 1 << 16
+    rhs, tau, _ = problems.seeded_rhs(p_t, n, 1.0, 42)
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(p_t), tau, n, coarsest=2)
+    # fp32 residuals bottom out near 1e-5 relative at this size: stop at 1e-4
+    cfg = tmg.CycleConfig(nu1=1, nu2=1, eps=1e-4)
+    u64, st64 = tmg.solve(hier, rhs, np.zeros_like(rhs), cfg)
+    depth = len(hier.levels)
+    plan = solver.get_plan(hier, 0, depth, solver.omegas_for(hier, cfg, depth), cfg, 1, nat.F32)
+    F = torch.from_numpy(rhs).float().cuda()[None]
+    U = torch.zeros_like(F)
+    it, norms, conv = plan.solve(F, U, [1e-12 * float(np.linalg.norm(rhs))], cfg.eps, cfg.max_iters)
+    u32 = U[0].double().cpu().numpy()
+    assert conv[0] and abs(int(it[0]) - st64.iterations) <= 1
+    # same iterates up to fp32 rounding: the first residual norms agree to 1e-4;
+    # the final solutions differ by at most the algebraic error at eps = 1e-4
+    # (the two may stop one cycle apart)
+    assert np.allclose(norms[0][:3], st64.residual_norms[:3], rtol=1e-4)
+    assert np.linalg.norm(u32 - u64) <= 1e-3 * np.linalg.norm(u64)

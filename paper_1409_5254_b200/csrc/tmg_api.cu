@@ -529,7 +529,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                 CK(cudaMalloc(&halo[l], sizeof(T) * (size_t)B * a.chunks * ROWW * NT + 16));
                 if (l == 0) CK(cudaMalloc(&halo0_alt, sizeof(T) * (size_t)B * a.chunks * ROWW * NT + 16));
             }
-            if (tl >= 2 && ROWW == 64 && sizeof(T) == 8 && n[0] % 128 == 0)
+            if (tl >= 2 && sizeof(T) == 8 && n[0] % (2 * ROWW) == 0 && pair_rows_ok())
                 CK(cudaMalloc(&fl1_alt, sizeof(T) * (size_t)B * n[1] * NT + 16));
         }
         if (leaf_rows0) {
@@ -831,7 +831,10 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             const char *e = getenv("TMG_NO_VFUSE");
             v = (e && *e && *e != '0') ? 0 : 1;
         }
-        return v == 1 && fuse_up_down() && fl1_alt && o.gamma == 1 && tl >= 2 && pk[0] == pk[1] &&
+        // one-slab lanes: only in the bandwidth regime (measured: B=16 x 2^22
+        // p_t=2 -3.5 %, latency-bound 2^20 +3.5 %)
+        const bool big = ROWW == 64 || (long long)B * n[0] >= (1LL << 22);
+        return v == 1 && big && fuse_up_down() && fl1_alt && o.gamma == 1 && tl >= 2 && pk[0] == pk[1] &&
                aligned16(f) && aligned16(u) && aligned16(fl[1]) && aligned16(fl1_alt) && aligned16(uA[2]);
     }
     // K_UP2DOWN (default with the up2 scheme; TMG_NO_FUSE=1 keeps the two passes)

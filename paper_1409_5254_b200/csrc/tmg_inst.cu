@@ -165,7 +165,7 @@ int stream_d_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const Stre
     }
 }
 
-// the finest pass with the level-1 up pass fused in (two-slab lanes, sparse
+// the finest pass with the level-1 up pass fused in (fp64, sparse
 // coupling only; -1 = not available for this (dtype, n_t): use the separate passes)
 template <typename T, int NT>
 int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
@@ -175,14 +175,10 @@ int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const Stre
         return -1;
     } else {
         if (finest) {
-            if constexpr (slabs_per_lane<T, NT>() != 2) return -1;
-            else
-            {
-                switch (perm) {
-                case P_ID: return v_by_nu<T, NT, P_ID, true>(L0, L1, a, a1, nu, s);
-                case P_ROT: return v_by_nu<T, NT, P_ROT, true>(L0, L1, a, a1, nu, s);
-                default: return v_by_nu<T, NT, P_GEN, true>(L0, L1, a, a1, nu, s);
-                }
+            switch (perm) {
+            case P_ID: return v_by_nu<T, NT, P_ID, true>(L0, L1, a, a1, nu, s);
+            case P_ROT: return v_by_nu<T, NT, P_ROT, true>(L0, L1, a, a1, nu, s);
+            default: return v_by_nu<T, NT, P_GEN, true>(L0, L1, a, a1, nu, s);
             }
         }
         switch (perm) {

@@ -722,7 +722,7 @@ template <typename T, int NT, bool FINEST = true> struct RowLayoutV {
     static constexpr int OFF_C2 = OFF_F1 + ROW;
     static constexpr int STAGE = OFF_C2 + HALF;
     static constexpr int ST = FINEST ? 2 : 3;
-    static constexpr int LB = 2;             // numpy leaves per flush (smem budget)
+    static constexpr int LB = P == 2 ? 2 : 1;  // numpy leaves per flush (smem budget)
     static constexpr int LEAFBUF = FINEST ? LB * 128 : 0;
     static constexpr int RSTRIDE = NT * NT + 2;
     static constexpr int RELEMS = P == 1 ? 2 * (2 * RSTRIDE) : 0;  // both levels' (R1, R2), one-slab lanes
@@ -744,7 +744,6 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     using Lay = RowLayoutV<T, NT, FINEST>;
     using S = Streamer<T, NT, NU, SPARSE, FINEST ? K_UP2DOWN : K_UP2, PERM>;
     using S1 = Streamer<T, NT, NU, SPARSE, K_UP2, PERM>;
-    static_assert(S::P == 2 || !FINEST, "the fused finest pass needs two-slab lanes");
     constexpr int P = S::P, W = 32 * P;
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_trigger();

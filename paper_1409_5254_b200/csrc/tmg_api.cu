@@ -781,7 +781,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             const char *e = getenv("TMG_NO_VPAIR");
             v = (e && *e && *e != '0') ? 0 : 1;
         }
-        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
+        return v == 1 && up2 && SP && o.gamma == 1 && o.nu1 <= 2 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
                sizeof(T) == 8 && n[l] % (2 * ROWW) == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
                aligned16(fl[l + 1]) && aligned16(uA[l]) && aligned16(uA[l + 2]);
     }
@@ -794,7 +794,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             const char *e = getenv("TMG_NO_DPAIR");
             v = (e && *e && *e != '0') ? 0 : 1;
         }
-        return v == 1 && up2 && SP && o.gamma == 1 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
+        return v == 1 && up2 && SP && o.gamma == 1 && o.nu1 <= 2 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
                sizeof(T) == 8 && n[l] % (2 * ROWW) == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
                aligned16(fl[l + 1]) && aligned16(fl[l + 2]) && (l != 1 || !fl1_alt || aligned16(fl1_alt));
     }
@@ -834,7 +834,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         // one-slab lanes: only in the bandwidth regime (measured: B=16 x 2^22
         // p_t=2 -3.5 %, latency-bound 2^20 +3.5 %)
         const bool big = ROWW == 64 || (long long)B * n[0] >= (1LL << 22);
-        return v == 1 && big && fuse_up_down() && fl1_alt && o.gamma == 1 && tl >= 2 && pk[0] == pk[1] &&
+        return v == 1 && big && fuse_up_down() && fl1_alt && o.gamma == 1 && o.nu1 <= 2 && tl >= 2 && pk[0] == pk[1] &&
                aligned16(f) && aligned16(u) && aligned16(fl[1]) && aligned16(fl1_alt) && aligned16(uA[2]);
     }
     // K_UP2DOWN (default with the up2 scheme; TMG_NO_FUSE=1 keeps the two passes)

@@ -109,10 +109,8 @@ int v_by_nu(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T
     switch (nu) {
     case 1: return launch_v<T, NT, 1, PERM, FINEST>(L0, L1, a, a1, s);
     case 2: return launch_v<T, NT, 2, PERM, FINEST>(L0, L1, a, a1, s);
-    case 3: return launch_v<T, NT, 3, PERM, FINEST>(L0, L1, a, a1, s);
-    case 4: return launch_v<T, NT, 4, PERM, FINEST>(L0, L1, a, a1, s);
     }
-    return -2;
+    return -1;
 }
 }  // namespace
 
@@ -139,13 +137,13 @@ template <typename T, int NT, int PERM>
 int d_by_nu(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a, const StreamArgs<T> &a1,
             int nu, cudaStream_t s)
 {
+    // the multi-level kernels are built for nu <= 2 (BASELINE's sweep counts;
+    // larger nu takes the per-level kernels) to bound the build time
     switch (nu) {
     case 1: return launch_d<T, NT, 1, PERM>(L0, L1, a, a1, s);
     case 2: return launch_d<T, NT, 2, PERM>(L0, L1, a, a1, s);
-    case 3: return launch_d<T, NT, 3, PERM>(L0, L1, a, a1, s);
-    case 4: return launch_d<T, NT, 4, PERM>(L0, L1, a, a1, s);
     }
-    return -2;
+    return -1;
 }
 }  // namespace
 

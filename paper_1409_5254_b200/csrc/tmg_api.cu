@@ -273,13 +273,13 @@ int launch_stream(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
 int chunk_rows(long long n, long long batch, int leaf_rows, int w, int stage)
 {
     const long long rows = (n + w - 1) / w;
-    // TMG_CHUNK_WAVES / TMG_CHUNK_MIN: tuning overrides (default 2 waves of
-    // 16 resident warps per SM, chunks of 2..64 rows; 2 waves measured best on
-    // the latency-bound 2^20-slab levels, large batches hit the 64-row cap)
+    // TMG_CHUNK_WAVES / TMG_CHUNK_MIN / TMG_CHUNK_MAX: tuning overrides (default 1 wave of
+    // 16 resident warps per SM, chunks of 2..64 rows; with the two-level
+    // kernels 1 wave is 2 % faster than 2 on config 2 p_t=3, neutral elsewhere)
     static int waves = -1, rmin = -1, rmax = -1;
     if (waves < 0) {
         const char *e = getenv("TMG_CHUNK_WAVES");
-        waves = e ? std::max(1, atoi(e)) : 2;
+        waves = e ? std::max(1, atoi(e)) : 1;
         const char *m = getenv("TMG_CHUNK_MIN");
         rmin = m ? std::max(1, atoi(m)) : 2;
         const char *x = getenv("TMG_CHUNK_MAX");

@@ -42,7 +42,12 @@ WORKLOADS = {
     "config2": dict(batch=1, n=1 << 20, p_t=1, T=1.0, nu=1),
     "config2_p3": dict(batch=1, n=1 << 20, p_t=3, T=1.0, nu=1),
     "config1": dict(batch=1, n=1 << 10, p_t=1, T=1.0, nu=1),
+    # BASELINE config 5: ONE fused pass (nu1 = 2 sweeps + residual +
+    # restriction) over N = 2^26 slabs, p_t = 3, u and f iid N(0, 1)
+    "config5": dict(batch=1, n=1 << 26, p_t=3, T=1.0, nu=2),
 }
+C5_METRIC = "fused down pass time-DoF/s (fp64) and % of HBM roofline"
+C5_BYTES = 3.5  # algorithmic bytes per fine slab, units of n_t * s
 
 
 # ---------------------------------------------------------------------------
@@ -160,6 +165,8 @@ def run_reference_arm(args, w):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    if args.workload == "config5":
+        return run_reference_c5(args, w, ws)
     import torch
     from paper_1409_5254_b200 import problems
     # same seeded inputs as the GPU arm (assembled on the host here)
@@ -192,6 +199,38 @@ def run_reference_arm(args, w):
             "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, w),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_c5(args, w, ws):
+    """Reference arm of config 5: the oracle's fused pass over a bounded
+    sample (2^22 of the 2^26 slabs) per step, all host threads."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    m = 1 << 22
+    nt = w["p_t"] + 1
+    rng = np.random.default_rng(0)
+    u = rng.standard_normal((m, nt))
+    f = rng.standard_normal((m, nt))
+    ops, r1, r2, om = c5_level(w)
+    times = []
+    for s_ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.down_pass(ops, r1, r2, om, u, f, nu=w["nu"])
+        if s_ >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    value = m * nt * len(times) / sum(times)
+    sample = (f"each step: the fused pass over {m} of the {w['n']} slabs by the C restatement of "
+              f"the reference (oracle/), {cores} threads")
+    line = {"impl": "reference", "metric": C5_METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config5 (bounded CPU sample)", "n_slabs": w["n"], "p_t": w["p_t"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -255,7 +294,222 @@ def kernel_roofline(times, n, nt, B, kind):
     return None, None, None
 
 
+GOLDEN = os.path.join(REPO, "tests", "golden", "golden.json")
+# golden solves of each workload: (batch slot, golden case name, batch index)
+PIN_CASES = {"config3": [(0, "config3_b0", 0), (1, "config3_b1", 1)],
+             "config2": [(0, "config2_p1", None)], "config2_p3": [(0, "config2_p3", None)]}
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def parity_pins(workload, ids):
+    """[(slot, golden case, host rhs)] for the batch slots holding golden
+    problems (only where this rank's problem ids include them)."""
+    from paper_1409_5254_b200 import problems
+    try:
+        with open(GOLDEN) as fh:
+            cases = {c["name"]: c for c in json.load(fh)["big_solves"]}
+    except OSError:
+        return []
+    out = []
+    for slot, name, bidx in PIN_CASES.get(workload, []):
+        if bidx is not None and (slot >= len(ids) or ids[slot] != bidx):
+            continue
+        c = cases[name]
+        rhs, _, _ = problems.seeded_rhs(c["p_t"], c["n"], c["T"], 42, c["batch_index"])
+        out.append((slot, c, rhs))
+    return out
+
+
+def check_pins(pins, U, stats):
+    """{case: {sha_rhs, sha_u, norms, iterations}} -- each True iff identical to
+    the reference's own solve of that problem (tests/golden/make_golden.py)."""
+    res = {}
+    for slot, c, rhs in pins:
+        st = stats[slot]
+        res[c["name"]] = {"sha_rhs": _sha(rhs) == c["sha_rhs"],
+                          "sha_u": _sha(U[slot].cpu().numpy()) == c["sha_u"],
+                          "norms": st.residual_norms == c["residual_norms"],
+                          "iterations": st.iterations == c["iterations"]}
+    res["all"] = bool(pins) and all(all(v.values()) for k, v in res.items())
+    return res
+
+
+def c5_level(w):
+    """(LevelDesc-ready operators) of config 5: tau = T / N = 2^-26, optimal omega."""
+    import paper_1409_5254_b200 as tmg
+    tau = w["T"] / w["n"]
+    basis = tmg.BasisSpec(w["p_t"])
+    ops = tmg.assemble_local(basis, tau)
+    r1, r2 = tmg.build_transfers(basis, tau)
+    return ops, r1, r2, tmg.optimal_omega(tmg.alpha(basis, tau))
+
+
+def run_config5(args, w):
+    """BASELINE config 5 through the C ABI's tmg_down: fp64 (the parity path)
+    with the reference's config-5 inputs on the first 2^16 slabs (their
+    outputs must hash to the reference's, tests/golden), seeded N(0,1)
+    elsewhere; fp32 beside it (normwise vs fp64)."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl")
+    from paper_1409_5254_b200 import _native as nat, problems
+    from paper_1409_5254_b200 import dist as tdist
+    L = nat.load()
+    n, nt, nu = w["n"], w["p_t"] + 1, w["nu"]
+    ops, r1, r2, om = c5_level(w)
+    d = nat.level_desc(ops, n, om, r1, r2)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5000 + rank)
+    u = torch.randn((n, nt), generator=gen, device="cuda", dtype=torch.float64)
+    f = torch.randn((n, nt), generator=gen, device="cuda", dtype=torch.float64)
+    npre = 1 << 16
+    up, fp = problems.kernel_inputs(npre, nt, 0)
+    u[:npre].copy_(torch.from_numpy(up))
+    f[:npre].copy_(torch.from_numpy(fp))
+    uo = torch.empty_like(u)
+    fc = torch.empty((n // 2, nt), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def step(dt, uu, ff, o, c):
+        nat.check(L.tmg_down(dt, ctypes.byref(d), P(ff), P(uu), P(o), P(c), 1, nu, None, sp), "tmg_down")
+
+    def timed(dt, uu, ff, o, c, k):
+        for _ in range(args.warmup):
+            step(dt, uu, ff, o, c)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            step(dt, uu, ff, o, c)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3
+
+    with ClockSampler(local) as clk:
+        elapsed = timed(0, u, f, uo, fc, args.steps)
+    el_max, dof = tdist.reduce_time_and_work(elapsed, float(n * nt * args.steps), device="cuda")
+    launch_s = elapsed / args.steps
+    peak, peak_kind = peak_hbm()
+    bytes_f64 = C5_BYTES * nt * 8 * n
+    parity = {"prefix_sha_u": _sha(uo[:npre].cpu().numpy()) == golden_c5()["sha_u"],
+              "prefix_sha_fc": _sha(fc[:npre // 2].cpu().numpy()) == golden_c5()["sha_fc"]}
+    # fp32 variant of the same pass (throughput variant; normwise bar 1e-5)
+    u32, f32 = u.float(), f.float()
+    uo32, fc32 = torch.empty_like(u32), torch.empty_like(fc, dtype=torch.float32)
+    el32 = timed(1, u32, f32, uo32, fc32, args.steps)
+    err_u = float(torch.linalg.norm(uo32.double() - uo) / torch.linalg.norm(uo))
+    err_fc = float(torch.linalg.norm(fc32.double() - fc) / torch.linalg.norm(fc))
+    parity["fp32_normwise_u"] = err_u
+    parity["fp32_normwise_fc"] = err_fc
+    parity["all"] = parity["prefix_sha_u"] and parity["prefix_sha_fc"] and max(err_u, err_fc) <= 1e-5
+    del u32, f32, uo32, fc32
+
+    # e2e: host buffers (pinned) in and out every step through the C ABI call
+    uh, fh = u.cpu().pin_memory(), f.cpu().pin_memory()
+    uoh, fch = torch.empty_like(uh).pin_memory(), torch.empty_like(fc, device="cpu").pin_memory()
+
+    def e2e():
+        u.copy_(uh, non_blocking=True)
+        f.copy_(fh, non_blocking=True)
+        step(0, u, f, uo, fc)
+        uoh.copy_(uo, non_blocking=True)
+        fch.copy_(fc, non_blocking=True)
+    e2e()
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(args.steps):
+        e2e()
+    g1.record(stream)
+    torch.cuda.synchronize()
+    e2e_s, e2e_dof = tdist.reduce_time_and_work(g0.elapsed_time(g1) * 1e-3,
+                                                float(n * nt * args.steps), device="cuda")
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = c5_cpu_sample(w, uh.numpy(), fh.numpy(), 1 << 22)
+    if rank == 0:
+        traffic = None
+        try:
+            with open(PROFILE_SUMMARY) as fh_:
+                traffic = json.load(fh_).get("config5", {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        line = {
+            "metric": C5_METRIC, "value": dof / el_max, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "config5: one fused pass (nu1=2 sweeps + residual + restriction) "
+                                   "over N=2^26 slabs, p_t=3, T=1 (tau=2^-26), optimal omega",
+                       "n_slabs": n, "p_t": w["p_t"], "nu": nu,
+                       "inputs": "u, f ~ N(0,1): first 2^16 slabs = the reference's config-5 "
+                                 "inputs (default_rng(0)), the rest torch.randn (seed 5000+rank)",
+                       "l2": "inputs larger than L2 (no flush)"},
+            "roofline": {"bound": "hbm", "achieved": bytes_f64 / launch_s / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_f64 / launch_s / 1e9 / peak,
+                         "traffic": traffic, "kernel": "stream_kernel<double,4,2,...,K_DOWN> (tmg_down)",
+                         "bytes_per_launch": bytes_f64, "launch_s": launch_s,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "fp32": {"launch_s": el32 / args.steps,
+                                  "achieved": bytes_f64 / 2 / (el32 / args.steps) / 1e9,
+                                  "frac": bytes_f64 / 2 / (el32 / args.steps) / 1e9 / peak}},
+            "e2e": {"value": e2e_dof / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * n * nt * 8,
+                    "d2h_bytes_per_step": n * nt * 8 + (n // 2) * nt * 8,
+                    "path": "pinned host u, f -> H2D -> tmg_down (C ABI) -> D2H u, f_coarse, one stream"},
+            "gpu_launches": args.steps,
+            "parity": parity,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def golden_c5():
+    with open(GOLDEN) as fh:
+        return json.load(fh)["config5"]
+
+
+def c5_cpu_sample(w, u, f, m, threads=None):
+    """The oracle's fused pass (C restatement of the reference order) over the
+    first m slabs, all host threads: {value (time-DoF/s), ...}."""
+    from oracle import oracle as O
+    if threads:
+        O.set_threads(threads)
+    cores = O.num_threads()
+    ops, r1, r2, om = c5_level(w)
+    uu, ff = np.ascontiguousarray(u[:m]), np.ascontiguousarray(f[:m])
+    O.down_pass(ops, r1, r2, om, uu[:1024], ff[:1024], nu=w["nu"])
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        O.down_pass(ops, r1, r2, om, uu, ff, nu=w["nu"])
+        reps += 1
+        if time.perf_counter() - t0 > 5.0 or reps >= 20:
+            break
+    secs = (time.perf_counter() - t0) / reps
+    nt = w["p_t"] + 1
+    return {"value": m * nt / secs, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"the fused pass over the first {m} of {w['n']} slabs by the C restatement of "
+                      f"the reference (oracle/), {cores} OpenMP threads, {reps} repetitions",
+            "gbs": C5_BYTES * nt * 8 * m / secs / 1e9, "seconds": secs}
+
+
 def run_gpu_arm(args, w):
+    if args.workload == "config5":
+        return run_config5(args, w)
     import torch
     import torch.distributed as dist
     ws, rank, local = dist_env()
@@ -270,6 +524,13 @@ def run_gpu_arm(args, w):
     from paper_1409_5254_b200 import dist as tdist
     ids = tdist.problem_ids(rank, ws, B) if B > 1 else [None]
     F = problems.seeded_rhs_batch_device(p_t, n, w["T"], 42, ids if B > 1 else (None,))
+    # parity pins: the golden problems of this workload (the reference's own
+    # solves, tests/golden) are assembled on the host exactly as the reference
+    # does and placed in the batch; their solutions are checked after the
+    # timed region
+    pins = parity_pins(args.workload, ids)
+    for slot, case, rhs in pins:
+        F[slot].copy_(torch.from_numpy(rhs))
     floors = [1e-12 * float(v) for v in torch.linalg.norm(F.reshape(B, -1), dim=1).cpu()]
     hier = make_hier(w)
     cfg = tmg.CycleConfig(nu1=w["nu"], nu2=w["nu"], eps=1e-8)
@@ -321,12 +582,15 @@ def run_gpu_arm(args, w):
         it, norms, conv = plan_h.solve_host(F_host, None, U_host, floors, cfg.eps, cfg.max_iters)
         return [type("S", (), {"iterations": int(k)}) for k in it]
 
+    # the golden problems' solutions of the last timed solve
+    parity = check_pins(pins, U, stats)
+
     e2e_step()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = args.steps
     dof_e2e = 0.0
     f0.record()
     for _ in range(e2e_steps):
@@ -396,6 +660,7 @@ def run_gpu_arm(args, w):
                     "host buffers: H2D f, solve (zero guess), D2H u; 16 pipelined sub-batches "
                     "(copy-in / copy-out streams, three compute streams) overlap copies with solves"},
             "gpu_launches": launches_per_step * args.steps,
+            "parity": parity,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -131,6 +131,27 @@ int tmg_resid_sqsum(int dtype, const tmg_level_desc *lev, const void *f, const v
 int tmg_trace_enable(int on);
 int64_t tmg_trace_read(char *buf, int64_t cap);
 
+/* ---- right-hand side (rhs_moments, dg.py:265-287) ---------------------------
+ * rhs[b][n][j] = sum_k fvals[b][n][k] * weights[j][k] (the fused multiply-add
+ * chain from +0 of numpy's `fvals @ weights.T`, dg.py:284), then
+ * rhs[b][0][j] += u0[b] * start[j] where u0[b] != 0 (dg.py:285-286).
+ * nodes[s] (left Radau nodes c_k), weights[n_t * s] (tau * basis_values * b,
+ * row-major) and start[n_t] (basis values at 0) are HOST arrays, the
+ * reference's own; fvals, u0 (NULL = no initial value) and rhs are device
+ * arrays.  s must equal n_t (the Radau rule, dg.py:276). */
+int tmg_rhs_samples(const double *fvals, const double *u0, const double *nodes, const double *weights,
+                    const double *start, int n_t, int s, double *rhs, int64_t n_slabs, int64_t batch,
+                    void *stream);
+/* The same moments of f(t) = sum_q amp[b][q] sin(freq[q] t / T + phase[b][q])
+ * at t = t0 + (n + nodes[k]) tau, evaluated in the kernel (one launch for the
+ * whole batch; freq[q] host, = 2 pi (q+1) as formed on the host).  CUDA's sin
+ * (<= 2 ulp) stands in for the host libm: a few ulp from the host assembly. */
+int tmg_rhs_sines(const double *amp, const double *phase, const double *u0, const double *freq, int n_terms,
+                  double T, double tau, double t0, const double *nodes, const double *weights,
+                  const double *start, int n_t, int s, double *rhs, int64_t n_slabs, int64_t batch,
+                  void *stream);
+const char *tmg_rhs_last_error(void);
+
 /* ---- solver plan (the cycle / iteration driver, multigrid.py:263-500) ----- */
 
 typedef struct tmg_plan tmg_plan;

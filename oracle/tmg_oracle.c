@@ -207,12 +207,18 @@ double tmo_pairwise_sum(const double *a, int64_t n)
  * (scipy-openblas, DYNAMIC_ARCH) on the Xeon host that produced the golden
  * vectors -- n=1: a0x0; n=2: fma(a0,x0,a1x1); n=3: fma(a2,x2,fma(a0,x0,a1x1));
  * n=4: (a0x0+a2x2)+(a1x1+a3x3); all results then get "+ 0.0" (rows of exact
- * zeros come out as +0).  variant 1: plain sequential mul/add.
+ * zeros come out as +0).  variant 1: plain sequential mul/add.  variant 2:
+ * sequential FMA chain t = fma(a_j, x_j, t).
  * Returns -1 status through *ok when the variant has no tree for n. */
 double tmo_blas_dot_row(const double *a, const double *x, int n, int variant, int *ok)
 {
     double t;
     *ok = 1;
+    if (variant == 2) {
+        t = a[0] * x[0];
+        for (int j = 1; j < n; ++j) t = fma(a[j], x[j], t);
+        return t + 0.0;
+    }
     if (variant == 1 || n > 4) {
         if (variant != 1) *ok = 0;
         t = a[0] * x[0];

@@ -10,7 +10,8 @@ from .assembly import (ALPHA_MIN, BasisSpec, BlockLU, GlobalSystem, LocalOperato
                        stability_function)
 from .hierarchy import CycleConfig, Level, SolveStats, TimeHierarchy
 from .solver import (DevicePlan, block_jacobi_sweep, forward_solve, measure_convergence_factor,
-                     measure_convergence_factors, rhs_moments_device,
-                     random_initial_guess, solve, solve_batched, two_grid_cycle, v_cycle)
+                     measure_convergence_factors, random_initial_guess, solve, solve_batched,
+                     two_grid_cycle, v_cycle)
+from .rhs import rhs_moments_device, rhs_moments_samples, rhs_moments_sines
 
 __version__ = "0.1.0"

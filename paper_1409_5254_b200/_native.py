@@ -17,7 +17,8 @@ REPO = os.path.dirname(HERE)
 LIB_PATH = os.environ.get("TMG_LIB") or os.path.join(HERE, "libtimemg_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(REPO, "include")
-MAXNT = 8
+MAXNT = 8          # field capacity of tmg_level_desc (TMG_MAXNT)
+KERNEL_MAXNT = 4   # n_t the kernels are instantiated for
 F64, F32 = 0, 1
 E_ARG, E_UNSUPPORTED, E_NOMEM = -1, -2, -3
 
@@ -60,27 +61,58 @@ def sources():
 
 # translation units: the C ABI / driver, and one kernel-instantiation unit per
 # (dtype, n_t) -- compiled in parallel, then linked into one shared library
-UNITS = [("tmg_api", "tmg_api.cu", [])] + [
-    (f"tmg_inst_{tn}_{nt}", "tmg_inst.cu", [f"-DTMG_T={t}", f"-DTMG_NT={nt}"])
-    for t, tn in (("double", "f64"), ("float", "f32")) for nt in (1, 2, 3, 4)]
+# (dtype, n_t, part): tmg_inst.cu's instantiations split in four parts
+UNITS = [("tmg_api", "tmg_api.cu", []), ("tmg_rhs", "tmg_rhs.cu", [])] + [
+    (f"tmg_inst_{tn}_{nt}_p{part}", "tmg_inst.cu", [f"-DTMG_T={t}", f"-DTMG_NT={nt}", f"-DTMG_PART={part}"])
+    for t, tn in (("double", "f64"), ("float", "f32")) for nt in (1, 2, 3, 4) for part in (0, 1, 2, 3)]
+# heaviest first, so the parallel build's tail is short
+UNITS.sort(key=lambda u: (0 if "f64" in u[0] else 1 if "inst" in u[0] else 2,
+                          -int(u[0].split("_")[3]) if "inst" in u[0] else 0))
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libtimemg_b200.so in-tree for sm_100a (skipped when up to date)."""
     from concurrent.futures import ThreadPoolExecutor
 
-    newest = max(os.path.getmtime(p) for p in sources() + [os.path.join(INCLUDE, "timemg_b200.h"),
-                                                          os.path.abspath(__file__)])
-    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
-        return LIB_PATH
+    stamp = LIB_PATH + ".flags"
+    flags_key = " ".join(NVCC_FLAGS)
+    same_flags = os.path.exists(stamp) and open(stamp).read() == flags_key
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     # objects stay outside the tree (they need not travel with the snapshot)
     objdir = os.environ.get("TMG_OBJDIR", "/tmp/tmg_b200_obj")
     os.makedirs(objdir, exist_ok=True)
 
+    def unit_newest(src):
+        """newest mtime of a unit's source and the headers it includes (recursively)."""
+        seen, todo = set(), [os.path.join(CSRC, src)]
+        while todo:
+            p = todo.pop()
+            if p in seen or not os.path.exists(p):
+                continue
+            seen.add(p)
+            for line in open(p, errors="replace"):
+                line = line.strip()
+                if line.startswith("#include \""):
+                    name = line.split('"')[1]
+                    todo += [os.path.join(CSRC, name), os.path.join(INCLUDE, name)]
+        return max(os.path.getmtime(p) for p in seen)
+
+    def stale(unit):
+        obj = os.path.join(objdir, unit[0] + ".o")
+        return force or not same_flags or not os.path.exists(obj) or \
+            os.path.getmtime(obj) < unit_newest(unit[1])
+
+    todo_units = [u for u in UNITS if stale(u)]
+    if not todo_units and os.path.exists(LIB_PATH) and \
+            os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(os.path.join(objdir, u[0] + ".o"))
+                                              for u in UNITS):
+        return LIB_PATH
+
     def compile_unit(unit):
         name, src, defs = unit
         obj = os.path.join(objdir, name + ".o")
+        if unit not in todo_units:
+            return obj
         extra = os.environ.get("TMG_NVCC_EXTRA", "").split()  # experiments: e.g. -DTMG_P2_WARPS=8
         cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", *defs, "-I", INCLUDE, "-I", CSRC, "-o", obj,
                os.path.join(CSRC, src)]
@@ -98,6 +130,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            *objs]
     subprocess.run(cmd, check=True)
     os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    with open(stamp, "w") as fh:
+        fh.write(flags_key)
     return LIB_PATH
 
 
@@ -107,7 +141,7 @@ EXPORTS = ("tmg_last_error", "tmg_version", "tmg_device_check", "tmg_sweep", "tm
            "tmg_down", "tmg_up", "tmg_coarse_solve", "tmg_resid_norm", "tmg_resid_sqsum", "tmg_trace_enable", "tmg_trace_read", "tmg_plan_create",
            "tmg_plan_create_multi",
            "tmg_plan_destroy", "tmg_plan_cycles", "tmg_plan_solve", "tmg_plan_solve_host",
-           "tmg_plan_stats", "tmg_plan_info")
+           "tmg_plan_stats", "tmg_plan_info", "tmg_rhs_samples", "tmg_rhs_sines", "tmg_rhs_last_error")
 
 
 def load():
@@ -143,6 +177,10 @@ def load():
     L.tmg_plan_solve_host.argtypes = [vp, vp, vp, vp, dp, ctypes.c_double, ci]
     L.tmg_plan_stats.argtypes = [vp, i32p, dp, i32p]
     L.tmg_plan_info.argtypes = [vp, i32p, i32p, i32p]
+    L.tmg_rhs_last_error.restype = ctypes.c_char_p
+    L.tmg_rhs_samples.argtypes = [vp, vp, dp, dp, dp, ci, ci, vp, i64, i64, vp]
+    L.tmg_rhs_sines.argtypes = [vp, vp, vp, dp, ci, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                dp, dp, dp, ci, ci, vp, i64, i64, vp]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or ci
     _lib = L
@@ -165,6 +203,11 @@ def level_desc(ops, n_slabs: int, omega: float = 1.0, r1=None, r2=None) -> Level
 
     d = LevelDesc()
     nt = int(ops.n_t)
+    if not 1 <= nt <= KERNEL_MAXNT:
+        # the kernels are instantiated for n_t = 1..4 (p_t <= 3); refuse before
+        # any copy into the fixed-size fields
+        raise NotImplementedError(f"n_t = {nt} (p_t = {nt - 1}): the GPU kernels support "
+                                  f"n_t in 1..{KERNEL_MAXNT}")
     d.n_t = nt
     d.n_slabs = int(n_slabs)
     d.omega = float(omega)
@@ -172,6 +215,8 @@ def level_desc(ops, n_slabs: int, omega: float = 1.0, r1=None, r2=None) -> Level
 
     def put(field, m):
         vals = np.ascontiguousarray(m, dtype=np.float64).ravel()
+        if vals.size != nt * nt or vals.size > len(field):
+            raise ValueError(f"level matrix of {vals.size} entries, expected {nt}x{nt}")
         ctypes.memmove(ctypes.addressof(field), vals.ctypes.data, vals.nbytes)
 
     put(d.minus_step, ops.minus_step_matrix)

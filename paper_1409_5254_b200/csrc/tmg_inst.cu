@@ -1,5 +1,13 @@
 // Kernel instantiations for one (dtype, n_t) pair: compile with
-//   -DTMG_T=double|float -DTMG_NT=1..4
+//   -DTMG_T=double|float -DTMG_NT=1..4 -DTMG_PART=0..3
+// The instantiations of a pair are split over four translation units so the
+// build runs them in parallel:
+//   part 0  the dispatcher, generic (runtime-flag) passes, down passes, tail,
+//           coarse solves
+//   part 1  up passes with separately stored pre-sweeps (K_UP, K_UPNORM) and
+//           K_UP2NORM
+//   part 2  the recomputing up passes (K_UP2, K_UP2DOWN)
+//   part 3  the multi-level kernels (vertical fusion, coarse pairs)
 #define TMG_INST_UNIT 1
 #include "tmg_launch.cuh"
 #include "tmg_stream.cuh"
@@ -8,8 +16,17 @@
 #ifndef TMG_T
 #error "define TMG_T and TMG_NT"
 #endif
+#ifndef TMG_PART
+#define TMG_PART -1  // all parts in one unit
+#endif
+#define TMG_IN_PART(k) (TMG_PART < 0 || TMG_PART == (k))
 
 namespace tmg {
+
+// one stream-kernel kind (all nu, all LU-permutation patterns); defined in
+// the part that owns the kind
+template <typename T, int NT, int KIND>
+int launch_kind(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int perm, cudaStream_t s);
 
 namespace {
 
@@ -60,6 +77,52 @@ int by_perm(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int perm, cu
 
 }  // namespace
 
+template <typename T, int NT, int KIND>
+int launch_kind(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int perm, cudaStream_t s)
+{
+    return by_perm<T, NT, KIND>(L, a, nu, perm, s);
+}
+
+#if TMG_IN_PART(0)
+template int launch_kind<TMG_T, TMG_NT, K_DOWN>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int,
+                                                int, cudaStream_t);
+template int launch_kind<TMG_T, TMG_NT, K_DOWNNORM>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &,
+                                                    int, int, cudaStream_t);
+#endif
+#if TMG_IN_PART(1)
+template int launch_kind<TMG_T, TMG_NT, K_UP>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
+                                              cudaStream_t);
+template int launch_kind<TMG_T, TMG_NT, K_UPNORM>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int,
+                                                  int, cudaStream_t);
+template int launch_kind<TMG_T, TMG_NT, K_UP2NORM>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int,
+                                                   int, cudaStream_t);
+#endif
+#if TMG_IN_PART(2)
+template int launch_kind<TMG_T, TMG_NT, K_UP2>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
+                                               cudaStream_t);
+template int launch_kind<TMG_T, TMG_NT, K_UP2DOWN>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int,
+                                                   int, cudaStream_t);
+#endif
+
+// kinds instantiated in other parts: no implicit instantiation here
+#define TMG_EXTERN_KIND(K)                                                                                    \
+    extern template int launch_kind<TMG_T, TMG_NT, K>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, \
+                                                      int, int, cudaStream_t);
+#if TMG_PART > 0
+TMG_EXTERN_KIND(K_DOWN)
+TMG_EXTERN_KIND(K_DOWNNORM)
+#endif
+#if TMG_PART == 0 || TMG_PART > 1
+TMG_EXTERN_KIND(K_UP)
+TMG_EXTERN_KIND(K_UPNORM)
+TMG_EXTERN_KIND(K_UP2NORM)
+#endif
+#if TMG_PART >= 0 && TMG_PART != 2
+TMG_EXTERN_KIND(K_UP2)
+TMG_EXTERN_KIND(K_UP2DOWN)
+#endif
+
+#if TMG_IN_PART(0)
 template <typename T, int NT>
 int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int kind, int perm, bool sparse,
                   cudaStream_t s)
@@ -70,18 +133,19 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
                       : by_nu<T, NT, false, K_GENERIC, P_GEN>(L, a, nu, s);
     }
     switch (kind) {
-    case K_DOWN: return by_perm<T, NT, K_DOWN>(L, a, nu, perm, s);
-    case K_UP: return by_perm<T, NT, K_UP>(L, a, nu, perm, s);
-    case K_UPNORM: return by_perm<T, NT, K_UPNORM>(L, a, nu, perm, s);
-    case K_DOWNNORM: return by_perm<T, NT, K_DOWNNORM>(L, a, nu, perm, s);
-    case K_UP2: return by_perm<T, NT, K_UP2>(L, a, nu, perm, s);
-    case K_UP2NORM: return by_perm<T, NT, K_UP2NORM>(L, a, nu, perm, s);
-    case K_UP2DOWN: return by_perm<T, NT, K_UP2DOWN>(L, a, nu, perm, s);
+    case K_DOWN: return launch_kind<T, NT, K_DOWN>(L, a, nu, perm, s);
+    case K_UP: return launch_kind<T, NT, K_UP>(L, a, nu, perm, s);
+    case K_UPNORM: return launch_kind<T, NT, K_UPNORM>(L, a, nu, perm, s);
+    case K_DOWNNORM: return launch_kind<T, NT, K_DOWNNORM>(L, a, nu, perm, s);
+    case K_UP2: return launch_kind<T, NT, K_UP2>(L, a, nu, perm, s);
+    case K_UP2NORM: return launch_kind<T, NT, K_UP2NORM>(L, a, nu, perm, s);
+    case K_UP2DOWN: return launch_kind<T, NT, K_UP2DOWN>(L, a, nu, perm, s);
     }
     return -1;
 }
 
 template <typename T, int NT> size_t stream_smem_bytes() { return RowLayout<T, NT, true, true>::SMEM_BYTES; }
+#endif
 
 namespace {
 template <typename T, int NT, int NU, int PERM, bool FINEST>
@@ -147,6 +211,7 @@ int d_by_nu(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T
 }
 }  // namespace
 
+#if TMG_IN_PART(3)
 // coarse down-pass pairs (two-slab lanes, fp64, sparse coupling; -1 = not available)
 template <typename T, int NT>
 int stream_d_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const StreamArgs<T> &a,
@@ -187,6 +252,9 @@ int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const Stre
     }
 }
 
+#endif  // part 3
+
+#if TMG_IN_PART(0)
 template <typename T, int NT> int tail_prepare(bool sparse, size_t smem)
 {
     cudaError_t e = sparse ? cudaFuncSetAttribute(tail_kernel<T, NT, true>,
@@ -226,15 +294,19 @@ template int coarse_scan_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, co
 template int stream_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
                                           int, bool, cudaStream_t);
 template size_t stream_smem_bytes<TMG_T, TMG_NT>();
+template int tail_prepare<TMG_T, TMG_NT>(bool, size_t);
+template int tail_launch<TMG_T, TMG_NT>(const TailArgs<TMG_T, TMG_NT> &, bool, unsigned, size_t, cudaStream_t);
+template int coarse_serial_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, bool, const TMG_T *, TMG_T *,
+                                                 long long, int, int, const int *, cudaStream_t);
+#endif  // part 0
+
+#if TMG_IN_PART(3)
 template int stream_d_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const LevelC<TMG_T, TMG_NT> &,
                                             const StreamArgs<TMG_T> &, const StreamArgs<TMG_T> &, int, int,
                                             cudaStream_t);
 template int stream_v_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const LevelC<TMG_T, TMG_NT> &,
                                             const StreamArgs<TMG_T> &, const StreamArgs<TMG_T> &, int, int,
                                             bool, cudaStream_t);
-template int tail_prepare<TMG_T, TMG_NT>(bool, size_t);
-template int tail_launch<TMG_T, TMG_NT>(const TailArgs<TMG_T, TMG_NT> &, bool, unsigned, size_t, cudaStream_t);
-template int coarse_serial_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, bool, const TMG_T *, TMG_T *,
-                                                 long long, int, int, const int *, cudaStream_t);
+#endif
 
 }  // namespace tmg

@@ -90,8 +90,9 @@ __device__ __forceinline__ double divq_nb(double a, double d, double rinv, unsig
 {
     double q0 = __dmul_rn(a, rinv);
     double q1 = __fma_rn(__fma_rn(-q0, d, a), rinv, q0);
-    const unsigned e = (unsigned)(__double2hiint(a) >> 20) & 0x7ffu;
-    bad |= (unsigned)(e - 123u >= 1800u);
+    // exponent field in place (one LOP3); the caller-side OR folds into a max
+    const unsigned e = (unsigned)__double2hiint(a) & 0x7ff00000u;
+    bad |= (unsigned)(e - (123u << 20) >= (1800u << 20));
     return __fma_rn(__fma_rn(-q1, d, a), rinv, q1);
 }
 __device__ __forceinline__ float divq_nb(float a, float d, float rinv, unsigned &bad)
@@ -160,7 +161,26 @@ __device__ __forceinline__ void bmat(const T *M, const T (&x)[NT], T (&o)[NT])
     }
 }
 
-template <typename T, int NT, bool SPARSE>
+// Signed zeros of the sparse coupling.  Row i >= 1 of the reference's
+// residual is r_i = ((A u)_i + f_i) + z_i with z_i = sum_j (+-0 * u_prev[j]) a
+// signed zero; adding it changes r_i only when (A u)_i + f_i is -0, which in
+// round-to-nearest needs f_i = -0.  So when no f_i (i >= 1) of the slabs at
+// hand is -0 ("SZ = false", checked once per row of slabs), z_i is skipped
+// and the predecessor's sign bits are not needed at all; otherwise (SZ =
+// true) they are tracked exactly as before.  Both give the reference's bits.
+template <typename T, int NT>
+__device__ __forceinline__ bool neg_zero_rows(const T (&f)[NT])
+{
+    bool any = false;
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int i = 1; i < NT; ++i)
+            any |= (unsigned long long)__double_as_longlong((double)f[i]) == 0x8000000000000000ull;
+    }
+    return any;
+}
+
+template <typename T, int NT, bool SPARSE, bool SZ = true>
 __device__ __forceinline__ Cpl<T, NT, SPARSE> make_cpl(const LevelC<T, NT> &L, const T (&u)[NT])
 {
     Cpl<T, NT, SPARSE> c;
@@ -176,8 +196,10 @@ __device__ __forceinline__ Cpl<T, NT, SPARSE> make_cpl(const LevelC<T, NT> &L, c
         for (int j = 1; j < NT; ++j) a = FP<T>::add(a, FP<T>::mul(L.C[j], u[j]));
         c.s = a;
         unsigned m = 0;
+        if constexpr (SZ) {
 #pragma unroll
-        for (int j = 0; j < NT; ++j) m |= FP<T>::sbit(u[j]) << j;
+            for (int j = 0; j < NT; ++j) m |= FP<T>::sbit(u[j]) << j;
+        }
         c.m = m;
     } else {
 #pragma unroll
@@ -209,13 +231,13 @@ __device__ __forceinline__ Cpl<T, NT, SPARSE> cpl_shfl_up(const Cpl<T, NT, SPARS
     return o;
 }
 
-template <typename T, int NT, bool SPARSE>
+template <typename T, int NT, bool SPARSE, bool SZ = true>
 __device__ __forceinline__ Cpl<T, NT, SPARSE> cpl_shfl(const Cpl<T, NT, SPARSE> &c, int src)
 {
     Cpl<T, NT, SPARSE> o;
     if constexpr (SPARSE) {
         o.s = shfl_t(c.s, src);
-        o.m = shfl_t(c.m, src);
+        o.m = SZ ? shfl_t(c.m, src) : 0u;
     } else {
 #pragma unroll
         for (int j = 0; j < NT; ++j) o.u[j] = shfl_t(c.u[j], src);
@@ -235,13 +257,13 @@ __device__ __forceinline__ void cpl_zero(Cpl<T, NT, SPARSE> &c)
     }
 }
 
-template <typename T, int NT, bool SPARSE>
+template <typename T, int NT, bool SPARSE, bool SZ = true>
 __device__ __forceinline__ void cpl_select(Cpl<T, NT, SPARSE> &dst, const Cpl<T, NT, SPARSE> &src,
                                            bool take)
 {
     if constexpr (SPARSE) {
         dst.s = take ? src.s : dst.s;
-        dst.m = take ? src.m : dst.m;
+        if constexpr (SZ) dst.m = take ? src.m : dst.m;
     } else {
 #pragma unroll
         for (int j = 0; j < NT; ++j) dst.u[j] = take ? src.u[j] : dst.u[j];
@@ -249,7 +271,7 @@ __device__ __forceinline__ void cpl_select(Cpl<T, NT, SPARSE> &dst, const Cpl<T,
 }
 
 // r = ((A u) + f) [+ N u_prev if has_prev]   (multigrid.py:159-165)
-template <typename T, int NT, bool SPARSE>
+template <typename T, int NT, bool SPARSE, bool SZ = true>
 __device__ __forceinline__ void residual(const LevelC<T, NT> &L, const T (&u)[NT], const T (&f)[NT],
                                          const Cpl<T, NT, SPARSE> &p, bool has_prev, T (&r)[NT])
 {
@@ -280,6 +302,7 @@ __device__ __forceinline__ void residual(const LevelC<T, NT> &L, const T (&u)[NT
     if constexpr (SPARSE) {
         T r0 = FP<T>::add(r[0], p.s);
         r[0] = has_prev ? r0 : r[0];
+        if constexpr (!SZ) return;  // no -0 among f[1..]: the zero terms change nothing
         const unsigned full = (1u << NT) - 1u;
 #pragma unroll
         for (int i = 1; i < NT; ++i) {
@@ -376,12 +399,18 @@ template <typename T, int NT> __device__ __forceinline__ T sqnorm(const T (&r)[N
 }
 
 // One row of `coupling @ x` as numpy/OpenBLAS computes it (multigrid.py:205).
-// variant 0: trees measured on the golden host (OpenBLAS 0.3.30); 1: sequential.
+// variant 0: trees measured on the golden host (OpenBLAS 0.3.30); 1: sequential;
+// 2: sequential FMA chain.  The host picks the variant by measuring its own
+// numpy (paper_1409_5254_b200/blas_tree.py).
 template <typename T, int NT>
 __device__ __forceinline__ T blas_dot(const T *a, const T (&x)[NT], int variant)
 {
     T t;
-    if (variant == 1 || NT > 4) {
+    if (variant == 2) {
+        t = FP<T>::mul(a[0], x[0]);
+#pragma unroll
+        for (int j = 1; j < NT; ++j) t = FP<T>::fma(a[j], x[j], t);
+    } else if (variant == 1 || NT > 4) {
         t = FP<T>::mul(a[0], x[0]);
 #pragma unroll
         for (int j = 1; j < NT; ++j) t = FP<T>::add(t, FP<T>::mul(a[j], x[j]));
@@ -464,13 +493,13 @@ enum PermKind { P_GEN = 0, P_ID = 1, P_ROT = 2 };
 
 // y_i = r_{perm[i]} with r = ((A u) + f) [+ N u_prev]: each row computed in
 // exactly the reference's order, just stored in the order the LU solve reads.
-template <typename T, int NT, bool SPARSE, int PERM>
+template <typename T, int NT, bool SPARSE, int PERM, bool SZ = true>
 __device__ __forceinline__ void residual_perm(const LevelC<T, NT> &L, const T (&u)[NT], const T (&f)[NT],
                                               const Cpl<T, NT, SPARSE> &p, bool has_prev, T (&y)[NT])
 {
     if constexpr (PERM == P_GEN || fast_fp<T>()) {
         T r[NT];
-        residual<T, NT, SPARSE>(L, u, f, p, has_prev, r);
+        residual<T, NT, SPARSE, SZ>(L, u, f, p, has_prev, r);
         if constexpr (PERM == P_ROT) {
 #pragma unroll
             for (int i = 0; i < NT; ++i) y[i] = r[(i + 1) % NT];
@@ -498,6 +527,10 @@ __device__ __forceinline__ void residual_perm(const LevelC<T, NT> &L, const T (&
             a = FP<T>::add(a, f[src]);
             T c;
             if constexpr (SPARSE) {
+                if (!SZ && src != 0) {  // zero term skipped (see neg_zero_rows)
+                    y[i] = a;
+                    continue;
+                }
                 c = (src == 0) ? p.s : FP<T>::zero(((p.m ^ L.cneg[src]) & full) == full);
             } else {
                 c = FP<T>::mul(L.C[src * NT], p.u[0]);
@@ -596,13 +629,13 @@ __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], 
 
 // J independent slabs (one per row of a stage) swept together: two dependency
 // chains per lane hide the fp64 latency of the strictly ordered arithmetic
-template <typename T, int NT, bool SPARSE, int PERM, int J>
+template <typename T, int NT, bool SPARSE, int PERM, int J, bool SZ = true>
 __device__ __forceinline__ void sweep_j(const LevelC<T, NT> &L, T (&u)[J][NT], const T (&f)[J][NT],
                                         const Cpl<T, NT, SPARSE> (&p)[J], const bool (&hp)[J])
 {
     T y[J][NT];
 #pragma unroll
-    for (int q = 0; q < J; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], p[q], hp[q], y[q]);
+    for (int q = 0; q < J; ++q) residual_perm<T, NT, SPARSE, PERM, SZ>(L, u[q], f[q], p[q], hp[q], y[q]);
     finish_j<T, NT, J>(L, u, y);
 }
 

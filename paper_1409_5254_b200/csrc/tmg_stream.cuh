@@ -253,12 +253,14 @@ template <typename T, int NT, bool WITH_C, bool LEAF> struct RowLayout {
     static constexpr int RELEMS = (P == 1 && NT >= 3) ? 2 * NT * NT + 2 : 0;
     static constexpr int RSTRIDE = NT * NT + 2;
     static constexpr size_t RBYTES = ((sizeof(T) * RELEMS + 15) / 16) * 16;
+    // signed-zero record (fp64): up to 3 nu + 1 = 13 exchanges per row
+    static constexpr size_t RECBYTES = sizeof(T) == 8 ? ((13 * NT * 4 + 15) / 16) * 16 : 0;
     // ring depth from the per-CTA budget of the CTA shape: 2..4 stages
     static constexpr int WARPS = CtaShape<T, NT>::WARPS;
-    static constexpr size_t WARP_CAP = CtaShape<T, NT>::CAP / WARPS - LBYTES - RBYTES;
+    static constexpr size_t WARP_CAP = CtaShape<T, NT>::CAP / WARPS - LBYTES - RBYTES - RECBYTES;
     static constexpr int ST_RAW = (int)(WARP_CAP / (sizeof(T) * STAGE));
     static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > SW_STAGES ? SW_STAGES : ST_RAW);
-    static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * ST + RBYTES + LBYTES;
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * STAGE * ST + RBYTES + LBYTES + RECBYTES;
     // mbarrier block (one 8-byte barrier per warp and stage), padded to 128 B
     static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
@@ -290,8 +292,15 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     // one slab per lane: this lane's transfer block (odd lanes R2, even lanes
     // R1) in registers for n_t <= 2, a per-warp shared-memory copy above
     static constexpr bool RREG = P == 1 && NT * NT * sizeof(T) <= 64;
+    // exact signed zeros of the sparse coupling (see neg_zero_rows): rows
+    // whose f has no -0 skip them; the others need the sign bits of the
+    // previous row's last slab at every exchange, which lane 31 leaves in
+    // `rec` (the high words of its slab: one store per exchange)
+    static constexpr bool TRACK = SPARSE && !fast_fp<T>();
+    static constexpr int NX = NPRE + NU + NPOST + 1;  // exchanges per row
     T Rm[RREG ? NT * NT : 1];
     const T *Rs;
+    unsigned *rec;           // [NX][NT] (TRACK)
     C carry[NPRE + NU + NPOST + 1];  // lane 0: predecessor data of the next row, per sweep
     T *leafbuf;              // per-warp numpy leaf buffer (SF_NORM_LEAF)
     int leaf_q;              // rows buffered in leafbuf
@@ -348,17 +357,43 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
 
     // predecessor data of the row's P slabs at sweep k: the lane's own earlier
     // slab, or (first slab) lane-1's last slab / the carry from the previous row
+    template <bool SZ>
     __device__ __forceinline__ void exchange(const T (&u)[P][NT], int k, C (&prev)[P])
     {
         C own[P];
 #pragma unroll
-        for (int q = 0; q < P; ++q) own[q] = make_cpl<T, NT, SPARSE>(L, u[q]);
-        C x = cpl_shfl<T, NT, SPARSE>(own[P - 1], (lane + 31) & 31);
+        for (int q = 0; q < P; ++q) own[q] = make_cpl<T, NT, SPARSE, SZ>(L, u[q]);
+        C x = cpl_shfl<T, NT, SPARSE, SZ>(own[P - 1], (lane + 31) & 31);
         prev[0] = x;
-        cpl_select<T, NT, SPARSE>(prev[0], carry[k], lane == 0);
+        cpl_select<T, NT, SPARSE, SZ>(prev[0], carry[k], lane == 0);
+        if constexpr (TRACK && SZ) {
+            // lane 0's predecessor is the previous row's last slab: its sign
+            // bits from the record (the carry holds only its coupling sum
+            // when that row skipped the signed zeros)
+            __syncwarp();
+            if (lane == 0) {
+                unsigned m = 0;
+#pragma unroll
+                for (int j = 0; j < NT; ++j) m |= (rec[k * NT + j] >> 31) << j;
+                prev[0].m = m;
+            }
+            __syncwarp();
+        }
 #pragma unroll
         for (int q = 1; q < P; ++q) prev[q] = own[q - 1];
         carry[k] = x;
+        if constexpr (TRACK) {
+            if (lane == 31) {
+                if constexpr (NT == 2) {
+                    *reinterpret_cast<uint2 *>(rec + k * NT) =
+                        make_uint2((unsigned)__double2hiint((double)u[P - 1][0]),
+                                   (unsigned)__double2hiint((double)u[P - 1][1]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) rec[k * NT + j] = (unsigned)__double2hiint((double)u[P - 1][j]);
+                }
+            }
+        }
     }
 
     // one row; slab0 = this lane's first slab.  INTERIOR: every slab exists
@@ -367,6 +402,33 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     template <bool INTERIOR>
     __device__ __forceinline__ void row(T (&u)[P][NT], const T (&f)[P][NT], const T (&uc)[NT], long long slab0,
                                         long long row_idx, bool warm, int b, T *uo, T *fco, bool zg)
+    {
+        if constexpr (TRACK) {
+            bool nz = false;
+#pragma unroll
+            for (int q = 0; q < P; ++q) nz |= neg_zero_rows<T, NT>(f[q]);
+            if (__any_sync(0xffffffffu, nz)) {
+                row_exact<INTERIOR>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
+                return;
+            }
+        }
+        row_impl<INTERIOR, false>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
+    }
+
+    // the rare rows with -0 in f (signed zeros tracked): one out-of-line copy
+    // per kernel instead of one per call site (compile time)
+    template <bool INTERIOR>
+    __device__ __noinline__ void row_exact(T (&u)[P][NT], const T (&f)[P][NT], const T (&uc)[NT],
+                                           long long slab0, long long row_idx, bool warm, int b, T *uo,
+                                           T *fco, bool zg)
+    {
+        row_impl<INTERIOR, true>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
+    }
+
+    template <bool INTERIOR, bool SZ>
+    __device__ __forceinline__ void row_impl(T (&u)[P][NT], const T (&f)[P][NT], const T (&uc)[NT],
+                                             long long slab0, long long row_idx, bool warm, int b, T *uo,
+                                             T *fco, bool zg)
     {
         bool valid[P], hp[P];
 #pragma unroll
@@ -382,8 +444,8 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                 continue;
             }
             C prev[P];
-            exchange(u, k, prev);
-            sweep_j<T, NT, SPARSE, PERM, P>(L, u, f, prev, hp);
+            exchange<SZ>(u, k, prev);
+            sweep_j<T, NT, SPARSE, PERM, P, SZ>(L, u, f, prev, hp);
         }
         if (has(SF_PROLONG)) {
 #pragma unroll
@@ -404,12 +466,12 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                 continue;
             }
             C prev[P];
-            exchange(u, NPRE + k, prev);
+            exchange<SZ>(u, NPRE + k, prev);
             if (NORM_IN && k == 0) {
                 // the first sweep's residual IS the input's residual: take its norm
                 T y[P][NT];
 #pragma unroll
-                for (int q = 0; q < P; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], prev[q], hp[q], y[q]);
+                for (int q = 0; q < P; ++q) residual_perm<T, NT, SPARSE, PERM, SZ>(L, u[q], f[q], prev[q], hp[q], y[q]);
                 if (!warm) {
                     T r[P][NT];
 #pragma unroll
@@ -418,7 +480,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                 }
                 finish_j<T, NT, P>(L, u, y);
             } else {
-                sweep_j<T, NT, SPARSE, PERM, P>(L, u, f, prev, hp);
+                sweep_j<T, NT, SPARSE, PERM, P, SZ>(L, u, f, prev, hp);
             }
         }
         if constexpr (NPOST > 0) {
@@ -439,11 +501,11 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
 #pragma unroll
             for (int k = 0; k < NPOST; ++k) {
                 C prev[P];
-                exchange(u, NPRE + NU + k, prev);
+                exchange<SZ>(u, NPRE + NU + k, prev);
                 if (k == 0) {
                     T y[P][NT];
 #pragma unroll
-                    for (int q = 0; q < P; ++q) residual_perm<T, NT, SPARSE, PERM>(L, u[q], f[q], prev[q], hp[q], y[q]);
+                    for (int q = 0; q < P; ++q) residual_perm<T, NT, SPARSE, PERM, SZ>(L, u[q], f[q], prev[q], hp[q], y[q]);
                     if (!warm) {
                         T r[P][NT];
 #pragma unroll
@@ -452,17 +514,17 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                     }
                     finish_j<T, NT, P>(L, u, y);
                 } else {
-                    sweep_j<T, NT, SPARSE, PERM, P>(L, u, f, prev, hp);
+                    sweep_j<T, NT, SPARSE, PERM, P, SZ>(L, u, f, prev, hp);
                 }
             }
         }
         if (need_r()) {
             C prev[P];
-            exchange(u, NPRE + NU + NPOST, prev);
+            exchange<SZ>(u, NPRE + NU + NPOST, prev);
             if (!warm) {
                 T r[P][NT];
 #pragma unroll
-                for (int q = 0; q < P; ++q) residual<T, NT, SPARSE>(L, u[q], f[q], prev[q], hp[q], r[q]);
+                for (int q = 0; q < P; ++q) residual<T, NT, SPARSE, SZ>(L, u[q], f[q], prev[q], hp[q], r[q]);
                 if (has(SF_WRITE_R)) {
 #pragma unroll
                     for (int q = 0; q < P; ++q)
@@ -551,8 +613,9 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     constexpr int ST = Lay::ST;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * ST;
     unsigned char *wbase = smem + Lay::BAR_BYTES + (size_t)warp * Lay::BYTES_PER_WARP;
-    T *ring = reinterpret_cast<T *>(wbase + Lay::RBYTES + Lay::LBYTES);
+    T *ring = reinterpret_cast<T *>(wbase + Lay::RBYTES + Lay::LBYTES + Lay::RECBYTES);
     st.leafbuf = reinterpret_cast<T *>(wbase + Lay::RBYTES);
+    st.rec = reinterpret_cast<unsigned *>(wbase + Lay::RBYTES + Lay::LBYTES);
     if constexpr (P == 1) {
         if (st.has(SF_RESTRICT) || prolong) {
             const bool odd = lane & 1;
@@ -727,7 +790,10 @@ template <typename T, int NT, bool FINEST = true> struct RowLayoutV {
     static constexpr int RSTRIDE = NT * NT + 2;
     static constexpr int RELEMS = P == 1 ? 2 * (2 * RSTRIDE) : 0;  // both levels' (R1, R2), one-slab lanes
     static constexpr int WARPS = CtaShape<T, NT>::WARPS;
-    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + LEAFBUF + RELEMS);
+    // signed-zero records (fp64, nu <= 2): 3 nu + 1 exchanges per fine row, 2 nu + 1 per coarse row
+    static constexpr int REC_FINE = 7 * NT, REC_COARSE = 5 * NT;
+    static constexpr size_t RECBYTES = sizeof(T) == 8 ? (((REC_FINE + REC_COARSE) * 4 + 15) / 16) * 16 : 0;
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + LEAFBUF + RELEMS) + RECBYTES;
     static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
 };
@@ -780,6 +846,11 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     st.lb = Lay::LB;
     T *u1row = reinterpret_cast<T *>(wbase) + Lay::LEAFBUF;
     T *ring = u1row + Lay::ROW;
+    {
+        unsigned *rec = reinterpret_cast<unsigned *>(wbase + Lay::BYTES_PER_WARP - Lay::RECBYTES);
+        st.rec = rec;
+        s1.rec = rec + Lay::REC_FINE;
+    }
     if constexpr (P == 1) {
         T *rs = ring + Lay::STAGE * Lay::ST;
         for (int i = lane; i < NT * NT; i += 32) {
@@ -928,7 +999,10 @@ template <typename T, int NT> struct RowLayoutD {
     static constexpr int RSTRIDE = NT * NT + 2;
     static constexpr int RELEMS = P == 1 ? 2 * (2 * RSTRIDE) : 0;
     static constexpr int WARPS = CtaShape<T, NT>::WARPS;
-    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + RELEMS);
+    // signed-zero records (fp64, nu <= 2): nu + 1 exchanges per row, both levels
+    static constexpr int REC_ONE = 3 * NT;
+    static constexpr size_t RECBYTES = sizeof(T) == 8 ? ((2 * REC_ONE * 4 + 15) / 16) * 16 : 0;
+    static constexpr size_t BYTES_PER_WARP = sizeof(T) * (STAGE * ST + ROW + RELEMS) + RECBYTES;
     static constexpr size_t BAR_BYTES = ((WARPS * ST * 8 + 127) / 128) * 128;
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
 };
@@ -970,6 +1044,11 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     unsigned char *wbase = smem + Lay::BAR_BYTES + (size_t)warp * Lay::BYTES_PER_WARP;
     T *c1row = reinterpret_cast<T *>(wbase);
     T *ring = c1row + Lay::ROW;
+    {
+        unsigned *rec = reinterpret_cast<unsigned *>(wbase + Lay::BYTES_PER_WARP - Lay::RECBYTES);
+        st.rec = rec;
+        s1.rec = rec + Lay::REC_ONE;
+    }
     if constexpr (P == 1) {
         // per-warp copies of both levels' (R1, R2); odd lanes use R2
         T *rs = ring + Lay::STAGE * Lay::ST;

@@ -78,11 +78,13 @@ class CycleConfig:
     """Solver parameters; the reference fields keep their meaning and defaults.
 
     Additions (not in the reference): ``cycle`` ("V", or "W" = gamma 2, see
-    DESIGN.md), ``coarse`` ("serial" = bitwise block forward substitution,
-    "scan" = parallel affine scan, "auto" = serial unless the coarsest level
-    is large) and ``dot_variant`` (the host-BLAS summation tree the reference's
-    coarse solve inherits).  ``workers`` and
-    ``min_slab`` are accepted for compatibility; the GPU ignores them.
+    DESIGN.md), ``coarse`` ("serial", the default: block forward substitution,
+    bitwise with the reference; "scan": parallel affine scan, ~1e-15 relative,
+    opt-in; "auto": serial unless the coarsest level has > 16384 slabs) and
+    ``dot_variant`` (the host-BLAS summation tree the reference's coarse solve
+    inherits; None = measured on this host by
+    blas_tree.py).  ``workers`` and ``min_slab`` are accepted for
+    compatibility; the GPU ignores them.
     """
 
     nu1: int = 2
@@ -95,8 +97,8 @@ class CycleConfig:
     workers: int = 1
     min_slab: int = 32768
     cycle: str = "V"
-    coarse: str = "auto"
-    dot_variant: int = 0
+    coarse: str = "serial"
+    dot_variant: object = None
 
     def __post_init__(self):
         if self.nu1 < 0 or self.nu2 < 0 or self.nu1 + self.nu2 < 1:
@@ -113,6 +115,8 @@ class CycleConfig:
             raise ValueError(f"cycle must be one of {CYCLES}, got {self.cycle!r}")
         if self.coarse not in COARSE_SOLVERS:
             raise ValueError(f"coarse must be one of {COARSE_SOLVERS}, got {self.coarse!r}")
+        if self.dot_variant is not None and self.dot_variant not in (0, 1, 2):
+            raise ValueError(f"dot_variant must be None, 0, 1 or 2, got {self.dot_variant!r}")
 
 
 @dataclasses.dataclass

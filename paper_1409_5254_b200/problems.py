@@ -56,24 +56,16 @@ def kernel_inputs(n_steps: int, n_t: int, seed: int = 0):
 
 def seeded_rhs_batch_device(p_t: int, n_steps: int, T: float = 1.0, seed=42, batch_indices=(0,),
                             device="cuda"):
-    """The seeded problems of ``seeded_rhs`` assembled on the GPU
-    (solver.rhs_moments_device).  Used to build large benchmark batches
-    quickly; values agree with the host assembly to a few ulp (the parity
-    tests use host inputs).  Returns a (B, n_steps, p_t + 1) float64 tensor."""
-    import torch
+    """The seeded problems of ``seeded_rhs`` assembled on the GPU in ONE launch
+    of the tmg_rhs_sines kernel (rhs.py): the forcing is evaluated in the
+    kernel, nothing but the 17 parameters per problem crosses PCIe.  Values
+    agree with the host assembly to a few ulp (CUDA's sin; the parity tests
+    and the bench's parity pins use host inputs).  Returns a
+    (B, n_steps, p_t + 1) float64 tensor."""
+    from .rhs import rhs_moments_sines
 
-    from .solver import rhs_moments_device
-
-    basis = BasisSpec(p_t)
-    out = torch.empty((len(batch_indices), n_steps, basis.n_t), dtype=torch.float64, device=device)
-    for i, b in enumerate(batch_indices):
-        a, phi, u0 = forcing_params(seed, b)
-
-        def f(t, a=a, phi=phi):
-            v = torch.zeros_like(t)
-            for k in range(8):
-                v += a[k] * torch.sin(2.0 * np.pi * (k + 1) * t / T + phi[k])
-            return v
-
-        out[i] = rhs_moments_device(f, basis, T / n_steps, n_steps, u0=u0, device=device)
-    return out
+    params = [forcing_params(seed, b) for b in batch_indices]
+    amp = np.stack([a for a, _, _ in params])
+    phase = np.stack([p for _, p, _ in params])
+    u0 = np.array([u for _, _, u in params])
+    return rhs_moments_sines(BasisSpec(p_t), T / n_steps, n_steps, amp, phase, T, u0)

@@ -26,6 +26,7 @@ import time
 import numpy as np
 
 from . import _native as nat
+from . import blas_tree
 from .hierarchy import CycleConfig, SolveStats, depth_of, level_omegas, max_ratio
 
 _COARSE = {"serial": 0, "scan": 1, "auto": 2}
@@ -70,6 +71,14 @@ def _is_host(x) -> bool:
         return False
 
 
+def _is_torch_cuda(x) -> bool:
+    try:
+        import torch
+        return torch.is_tensor(x) and x.is_cuda
+    except ImportError:
+        return False
+
+
 def _host_ptr(x) -> int:
     if isinstance(x, np.ndarray):
         return x.ctypes.data
@@ -90,6 +99,55 @@ def _host_array(x, copy: bool):
 
 def _check_device():
     nat.check(nat.load().tmg_device_check(0), "timemg_b200 needs a CUDA device (B200, sm_100a)")
+
+
+def _to_numpy(x):
+    """numpy view of a numpy array, scalar, list or (CPU or CUDA) torch tensor."""
+    if isinstance(x, np.ndarray):
+        return x
+    try:
+        import torch
+        if torch.is_tensor(x):
+            return x.detach().cpu().numpy()
+    except ImportError:
+        pass
+    return np.asarray(x, dtype=np.float64)
+
+
+def _host_block(x, shape, what: str, copy: bool):
+    """C-contiguous float64 host array of exactly ``shape``.  Anything numpy
+    broadcasts to that shape is accepted, as the reference's assignments
+    ``ws.u[0][0][:] = u_init`` / ``ws.f[0][:] = f`` do (multigrid.py:437-438);
+    anything else raises ValueError before a pointer reaches the C ABI."""
+    if _is_host(x) and tuple(x.shape) == shape:
+        return _host_array(x, copy)
+    src = _to_numpy(x)
+    out = np.empty(shape, dtype=np.float64)
+    try:
+        out[...] = src
+    except ValueError as e:
+        raise ValueError(f"{what} of shape {np.shape(src)} does not broadcast to {shape}") from e
+    return out
+
+
+def _dev_block(x, shape, what: str):
+    """(float64 CUDA tensor of exactly ``shape``, was_torch); broadcasts like
+    the reference's assignments, ValueError otherwise."""
+    torch = _torch()
+    was_t = torch.is_tensor(x)
+    t = x.to(device="cuda", dtype=torch.float64) if was_t else \
+        torch.from_numpy(np.ascontiguousarray(_to_numpy(x), dtype=np.float64)).to("cuda")
+    if tuple(t.shape) != shape:
+        try:
+            t = t.expand(shape)
+        except RuntimeError as e:
+            raise ValueError(f"{what} of shape {tuple(t.shape)} does not broadcast to {shape}") from e
+    return t.contiguous(), was_t
+
+
+def _check_floors(floors, B):
+    fl = np.ascontiguousarray(np.broadcast_to(np.asarray(floors, dtype=np.float64), (B,)))
+    return fl
 
 
 def _out(t, was_torch):
@@ -126,7 +184,7 @@ class DevicePlan:
         self.n_t = flat[0].n_t
         self.dtype = dtype
         opts = nat.PlanOpts(dtype, config.nu1, config.nu2, 2 if config.cycle == "W" else 1,
-                            _COARSE[config.coarse], int(config.dot_variant), int(use_graph),
+                            _COARSE[config.coarse], blas_tree.resolve(config.dot_variant), int(use_graph),
                             int(TAIL_MAX))
         self._h = ctypes.c_void_p()
         create = lib.tmg_plan_create if multi is None else lib.tmg_plan_create_multi
@@ -195,7 +253,7 @@ def omegas_for(hier, config, depth):
 
 def get_plan(hier, level0, depth, omegas, config, batch, dtype=nat.F64):
     key = (level0, depth, tuple(omegas), config.nu1, config.nu2, config.cycle, config.coarse,
-           config.dot_variant, batch, dtype, TAIL_MAX)
+           blas_tree.resolve(config.dot_variant), batch, dtype, TAIL_MAX)
     cache = hier.__dict__.setdefault("_tmg_plans", {})
     plan = cache.get(key)
     if plan is None:
@@ -270,15 +328,16 @@ def _forward_solve_dev(ops, n, fd, config, batch=1):
     d = nat.level_desc(ops, n)
     method = {"serial": 0, "scan": 1}.get(config.coarse, 1 if n > SCAN_AUTO_MIN else 0)
     nat.check(nat.load().tmg_coarse_solve(nat.F64, ctypes.byref(d), _ptr(fd), _ptr(u), batch, method,
-                                          int(config.dot_variant), _stream()), "tmg_coarse_solve")
+                                          blas_tree.resolve(config.dot_variant), _stream()),
+              "tmg_coarse_solve")
     return u
 
 
-def forward_solve(system, rhs, method: str = "scan"):
+def forward_solve(system, rhs, method: str = "serial"):
     """Exact solve of the block lower-bidiagonal system on the GPU
-    (dg.py:290-303).  method "serial": block forward substitution, bitwise
-    with the reference's coarse solve (one thread per problem); "scan": the
-    parallel associative scan of the rank-1 slab recurrence (~1e-15 relative).
+    (dg.py:290-303).  method "serial" (default): block forward substitution,
+    bitwise with the reference; "scan" (opt-in): the parallel associative scan
+    of the rank-1 slab recurrence (~1e-15 relative, not bitwise).
     rhs: (n_steps, n_t) or (B, n_steps, n_t); numpy in -> numpy out."""
     if getattr(system, "periodic", False):
         raise ValueError("forward substitution requires a non-periodic system")
@@ -309,14 +368,17 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
     Returns (u, SolveStats); non-convergence is a flag, not an exception."""
     config = config or CycleConfig()
     depth = depth_of(hier, config)
+    shape = (hier.finest.n_steps, hier.finest.ops.n_t)
     if u_init is None:
         u_init = random_initial_guess(hier, config.seed)
-    if depth >= 2 and _is_host(f):
-        # numpy (host) arrays: the C ABI's host-buffer entry point, no torch
+    if depth >= 2 and (_is_host(f) or not _is_torch_cuda(f)):
+        # host arrays (numpy, CPU torch, scalars): the C ABI's host-buffer
+        # entry point, no torch.  floor = 1e-12 ||f|| of f as given
+        # (multigrid.py:445), before broadcasting.
         _check_device()
-        fh = _host_array(f, copy=False)
-        uh = _host_array(u_init, copy=True)
-        floor = 1e-12 * float(np.linalg.norm(np.asarray(f, dtype=np.float64)))
+        fh = _host_block(f, shape, "f", copy=False)
+        uh = _host_block(u_init, shape, "u_init", copy=True)
+        floor = 1e-12 * float(np.linalg.norm(_to_numpy(f).astype(np.float64, copy=False)))
         plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, 1)
         t0 = time.perf_counter()
         it, norms, conv = plan.solve_host(fh, uh, uh, [floor], config.eps, config.max_iters)
@@ -327,16 +389,17 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
                               times=_times(elapsed), converged=bool(conv[0]), seed=config.seed,
                               workers=config.workers)
     torch = _torch()
-    fd, was_t = _dev(f)
+    fd, was_t = _dev_block(f, shape, "f")
     if depth < 2:
         u = _forward_solve_dev(hier.finest.ops, hier.finest.n_steps, fd, config)
         stats = SolveStats(iterations=0, residual_norms=[0.0], factor=float("nan"),
                            times=_times(0.0), converged=True, seed=config.seed,
                            workers=config.workers)
         return _out(u, was_t), stats
-    ud, _ = _dev(u_init)
-    ud = ud.clone()
-    floor = _floor_of(f)
+    ud, _ = _dev_block(u_init, shape, "u_init")
+    if torch.is_tensor(u_init) and ud.data_ptr() == u_init.data_ptr():
+        ud = ud.clone()
+    floor = _floor_of(f if torch.is_tensor(f) else _to_numpy(f))
     omegas = omegas_for(hier, config, depth)
     plan = get_plan(hier, 0, depth, omegas, config, 1)
     torch.cuda.synchronize()
@@ -360,38 +423,43 @@ def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None, inp
     depth = depth_of(hier, config)
     if depth < 2:
         raise ValueError("solve_batched needs at least 2 levels")
-    if _is_host(F):
+    N, nt = hier.finest.n_steps, hier.finest.ops.n_t
+    if len(getattr(F, "shape", ())) != 3 or tuple(F.shape[1:]) != (N, nt):
+        raise ValueError(f"F must have shape (B, {N}, {nt}), got {tuple(getattr(F, 'shape', ()))}")
+    B = int(F.shape[0])
+    shape = (B, N, nt)
+    if B < 1:
+        raise ValueError("solve_batched needs at least one problem")
+    if not _is_torch_cuda(F):
         # host buffers (numpy / CPU torch, ideally pinned): copies inside the C ABI
         _check_device()
-        Fh = _host_array(F, copy=False)
-        B = Fh.shape[0]
+        Fh = _host_block(F, shape, "F", copy=False)
         if U0 is None:
-            Uin, Uh = None, np.empty(tuple(Fh.shape))
+            Uin, Uh = None, np.empty(shape)
         else:
-            Uh = _host_array(U0, copy=not inplace)
+            host_u0 = _is_host(U0) and tuple(U0.shape) == shape
+            Uh = _host_block(U0, shape, "U0", copy=not (inplace and host_u0))
             Uin = Uh
         if floors is None:
             floors = [1e-12 * float(np.linalg.norm(np.asarray(Fh[b], dtype=np.float64)))
                       for b in range(B)]
+        floors = _check_floors(floors, B)
         plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, B)
         t0 = time.perf_counter()
         it, norms, conv = plan.solve_host(Fh, Uin, Uh, floors, config.eps, config.max_iters)
         elapsed = time.perf_counter() - t0
         return Uh, _batched_stats(it, norms, conv, elapsed, config)
     torch = _torch()
-    Fd, was_t = _dev(F)
-    B = Fd.shape[0]
+    Fd, was_t = _dev_block(F, shape, "F")
     if U0 is None:
         Ud = torch.zeros_like(Fd)
     else:
-        Ud, _ = _dev(U0)
+        Ud, _ = _dev_block(U0, shape, "U0")
         if not (inplace and torch.is_tensor(U0) and Ud.data_ptr() == U0.data_ptr()):
             Ud = Ud.clone()
     if floors is None:
-        if torch.is_tensor(F):
-            floors = [1e-12 * float(v) for v in torch.linalg.norm(Fd.reshape(B, -1), dim=1).cpu()]
-        else:
-            floors = [1e-12 * float(np.linalg.norm(F[b])) for b in range(B)]
+        floors = [1e-12 * float(v) for v in torch.linalg.norm(Fd.reshape(B, -1), dim=1).cpu()]
+    floors = _check_floors(floors, B)
     omegas = omegas_for(hier, config, depth)
     plan = get_plan(hier, 0, depth, omegas, config, B)
     torch.cuda.synchronize()
@@ -450,25 +518,3 @@ def measure_convergence_factors(basis, taus, nu=1, n_steps: int = 1024, damping=
     _check_device()
     it, norms, conv = plan.solve_host(F, U, U, np.zeros(len(hiers)), eps, min(max_iters, 250))
     return [max_ratio([float(v) for v in norms[b, :int(it[b]) + 1]]) for b in range(len(hiers))]
-
-
-def rhs_moments_device(f, basis, tau: float, n_steps: int, u0: float = 0.0, t0: float = 0.0,
-                       device: str = "cuda"):
-    """rhs_moments (dg.py:265-287) evaluated on the GPU: ``f`` takes a float64
-    CUDA tensor of times and returns values of the same shape (torch ops).
-    Left Radau quadrature of order 2 p_t + 1, u0 folded into slab 0.  Agrees
-    with the host assembly to a few ulp (transcendentals differ between numpy
-    and CUDA); returns a (n_steps, n_t) float64 CUDA tensor."""
-    torch = _torch()
-    from .assembly import basis_values, radau_rule
-    rule = radau_rule(basis.n_t)
-    weights = torch.from_numpy(tau * basis_values(basis, rule.c) * rule.b).to(device)
-    c = torch.from_numpy(rule.c).to(device)
-    times = t0 + (torch.arange(n_steps, device=device, dtype=torch.float64)[:, None] + c[None, :]) * tau
-    fv = f(times)
-    if not torch.is_tensor(fv) or fv.shape != times.shape:
-        raise TypeError("f must map a (n_steps, s) float64 tensor to values of the same shape")
-    rhs = fv.to(torch.float64) @ weights.T
-    if u0 != 0.0:
-        rhs[0] += u0 * torch.from_numpy(basis_values(basis, np.array([0.0]))[:, 0]).to(device)
-    return rhs

@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU-box profiling recipe for the headline (BASELINE config 3), one GPU:
-#   1. bench.py (the JSON line, CPU baseline included)
+#   1. (bench.py itself runs in scripts/gpu_round.sh)
 #   2. ncu launch list of bench.py (gpu__time_duration per launch, serialised)
 #   3. ncu --set full of the two dominant kernels of one solve (the finest
 #      level's vertically fused pass, stream_kernel_v<..., FINEST>; the largest
@@ -11,8 +11,6 @@ set -u
 TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 900 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
-echo "bench rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/${TAG}_launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu \
     > $OUT/${TAG}_ncu_bench.log 2>&1

@@ -66,3 +66,22 @@ def test_level_desc_packing():
     assert list(d.minus_step[:9]) == list(np.asarray(ops.minus_step_matrix).ravel())
     assert list(d.r2[:9]) == list(r2.ravel())
     assert list(d.perm[:3]) == list(ops.lu.perm)
+
+
+def test_level_desc_rejects_unsupported_degree():
+    from paper_1409_5254_b200 import assemble_local, BasisSpec
+    with pytest.raises(NotImplementedError):
+        nat.level_desc(assemble_local(BasisSpec(4), 0.1), 8)  # n_t = 5: no kernels
+    with pytest.raises(NotImplementedError):
+        nat.level_desc(assemble_local(BasisSpec(8), 0.1), 8)  # n_t = 9 > TMG_MAXNT
+
+
+def test_rhs_entry_points_validate_without_gpu(lib):
+    import numpy as np
+    dp = ctypes.POINTER(ctypes.c_double)
+    z = np.zeros(16)
+    p = z.ctypes.data_as(dp)
+    rc = lib.tmg_rhs_samples(None, None, p, p, p, 9, 9, None, 4, 1, None)
+    assert rc == nat.E_ARG and b"n_t" in lib.tmg_rhs_last_error()
+    rc = lib.tmg_rhs_sines(None, None, None, p, 8, -1.0, 0.1, 0.0, p, p, p, 2, 2, None, 4, 1, None)
+    assert rc == nat.E_ARG

@@ -422,6 +422,7 @@ def test_measure_convergence_factors_batched(golden):
 
 
 def test_rhs_moments_device_close_to_host():
+    """torch-evaluated forcing + the tmg_rhs_samples kernel vs the host quadrature."""
     import torch
     a, phi, u0 = problems.forcing_params(42)
     for p_t in range(4):

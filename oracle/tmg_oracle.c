@@ -258,6 +258,39 @@ int tmo_forward_substitute(const tmo_level *L, const double *rhs, double *out, i
     return ok ? 0 : 1;
 }
 
+/* The exact solution of the same block system (K+M) u_k = f_k + N u_{k-1}
+ * (dg.py:290-303) in extended precision (x87 long double, 64-bit mantissa):
+ * the yardstick for the parallel-scan solve, whose association differs from
+ * the serial sweep's -- both are compared with this instead of with each
+ * other when the recurrence is ill-conditioned (alpha -> 1 for small tau).
+ * Not a restatement of reference arithmetic; test infrastructure only. */
+int tmo_forward_substitute_ld(const tmo_level *L, const double *rhs, double *out, int64_t n)
+{
+    const int nt = L->nt;
+    long double prev[TMO_MAXNT] = {0};
+    for (int64_t k = 0; k < n; ++k) {
+        long double y[TMO_MAXNT], b[TMO_MAXNT];
+        for (int i = 0; i < nt; ++i) {
+            long double c = 0.0L;
+            if (k > 0)
+                for (int j = 0; j < nt; ++j) c += (long double)L->C[i * nt + j] * prev[j];
+            b[i] = (long double)rhs[k * nt + i] + c;
+        }
+        for (int i = 0; i < nt; ++i) y[i] = b[L->perm[i]];
+        for (int i = 1; i < nt; ++i)
+            for (int j = 0; j < i; ++j) y[i] -= (long double)L->lu[i * nt + j] * y[j];
+        for (int i = nt - 1; i >= 0; --i) {
+            for (int j = i + 1; j < nt; ++j) y[i] -= (long double)L->lu[i * nt + j] * y[j];
+            y[i] /= (long double)L->lu[i * nt + i];
+        }
+        for (int i = 0; i < nt; ++i) {
+            prev[i] = y[i];
+            out[k * nt + i] = (double)y[i];
+        }
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------------- cycles */
 
 typedef struct {

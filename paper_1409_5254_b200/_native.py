@@ -62,12 +62,17 @@ def sources():
 # translation units: the C ABI / driver, and one kernel-instantiation unit per
 # (dtype, n_t) -- compiled in parallel, then linked into one shared library
 # (dtype, n_t, part): tmg_inst.cu's instantiations split in four parts
+# (dtype, n_t, part): tmg_inst.cu's instantiations split in four parts, plus
+# the tail engine and coarse solves (tmg_inst_tail.cu)
+_TYPES = (("double", "f64"), ("float", "f32"))
 UNITS = [("tmg_api", "tmg_api.cu", []), ("tmg_rhs", "tmg_rhs.cu", [])] + [
     (f"tmg_inst_{tn}_{nt}_p{part}", "tmg_inst.cu", [f"-DTMG_T={t}", f"-DTMG_NT={nt}", f"-DTMG_PART={part}"])
-    for t, tn in (("double", "f64"), ("float", "f32")) for nt in (1, 2, 3, 4) for part in (0, 1, 2, 3)]
+    for t, tn in _TYPES for nt in (1, 2, 3, 4) for part in (0, 1, 2, 3)] + [
+    (f"tmg_inst_{tn}_{nt}_tail", "tmg_inst_tail.cu", [f"-DTMG_T={t}", f"-DTMG_NT={nt}"])
+    for t, tn in _TYPES for nt in (1, 2, 3, 4)]
 # heaviest first, so the parallel build's tail is short
 UNITS.sort(key=lambda u: (0 if "f64" in u[0] else 1 if "inst" in u[0] else 2,
-                          -int(u[0].split("_")[3]) if "inst" in u[0] else 0))
+                          -int(u[0].split("_")[3]) if "inst" in u[0] else 0, u[0]))
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -202,13 +202,62 @@ template <typename T, int NT> LevelC<T, NT> make_level(const tmg_level_desc &d)
         for (int j = i + 1; j < NT; ++j) y[i] -= d.lu[i * NT + j] * y[j];
         y[i] /= d.lu[i * NT + i];
     }
-    double al = 0.0;
-    for (int j = 0; j < NT; ++j) al += e[j] * y[j];
+    // alpha = e . LU^-1 c, the recurrence's multiplier, in double-double: the
+    // scan applies it ~N times, so its rounding must not be systematic at
+    // 1e-16 (tmg_scan.cuh)
+    auto two_prod = [](double a, double b, double &err) {
+        const double p = a * b;
+        err = std::fma(a, b, -p);
+        return p;
+    };
+    auto two_sum = [](double a, double b, double &err) {
+        const double s = a + b, bb = s - a;
+        err = (a - (s - bb)) + (b - bb);
+        return s;
+    };
+    double yh[NT], yl[NT];  // LU^-1 c in double-double
+    for (int i = 0; i < NT; ++i) {
+        yh[i] = c[d.perm[i]];
+        yl[i] = 0.0;
+    }
+    auto dd_sub_prod = [&](int i, double m, int j) {  // y_i -= m * y_j
+        double pe;
+        const double p = two_prod(m, yh[j], pe);
+        const double pl = pe + m * yl[j];
+        double se;
+        const double sh = two_sum(yh[i], -p, se);
+        const double sl = se + (yl[i] - pl);
+        yh[i] = sh + sl;
+        yl[i] = sl - (yh[i] - sh);
+    };
+    for (int i = 1; i < NT; ++i)
+        for (int j = 0; j < i; ++j) dd_sub_prod(i, d.lu[i * NT + j], j);
+    for (int i = NT - 1; i >= 0; --i) {
+        for (int j = i + 1; j < NT; ++j) dd_sub_prod(i, d.lu[i * NT + j], j);
+        const double dv = d.lu[i * NT + i];
+        const double q = yh[i] / dv;  // (yh + yl) / dv: one correction step
+        double pe;
+        const double p = two_prod(q, dv, pe);
+        const double r = ((yh[i] - p) - pe + yl[i]) / dv;
+        yh[i] = q + r;
+        yl[i] = r - (yh[i] - q);
+    }
+    double ah = 0.0, alo = 0.0;
+    for (int j = 0; j < NT; ++j) {
+        double pe;
+        const double p = two_prod(e[j], yh[j], pe);
+        double se;
+        const double sh = two_sum(ah, p, se);
+        alo += se + pe + e[j] * yl[j];
+        ah = sh;
+    }
+    const double al = ah + alo;
     for (int j = 0; j < NT; ++j) {
         L.ce[j] = (T)e[j];
-        L.cw[j] = (T)y[j];
+        L.cw[j] = (T)(yh[j] + yl[j]);
     }
     L.calpha = (T)al;
+    L.calpha_lo = (ah - (double)L.calpha) + alo;  // calpha + calpha_lo = alpha to ~1e-32
     L.scan_ok = ok ? 1 : 0;
     return L;
 }
@@ -413,10 +462,11 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         cudaFree(fl1_alt);
         cudaFree(d_levels);
         if (d_trace) {
-            std::vector<unsigned long long> tr(6 * MAXLEV);
+            std::vector<unsigned long long> tr(10 * MAXLEV);
             cudaMemcpy(tr.data(), d_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost);
-            const char *names[6] = {"sweep", "restrict", "prolong", "coarse", "norm", "warp"};
-            for (int k = 0; k < 6; ++k)
+            const char *names[10] = {"down", "-", "up", "coarse", "norm", "down.enter", "down.loads",
+                                     "down.compute", "down.stores", "down.leave"};
+            for (int k = 0; k < 10; ++k)
                 for (int l = 0; l < MAXLEV; ++l)
                     if (tr[k * MAXLEV + l]) fprintf(stderr, "tail-trace %s L%d %llu\n", names[k], l, tr[k * MAXLEV + l]);
             cudaFree(d_trace);
@@ -482,9 +532,9 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         const size_t smem_cap = 200 * 1024;
         // measured on config 2 (N = 2^20): 1024 (n_t <= 2) and 512 (n_t >= 3) beat 2048 / 1024 by 5-6 %
         long long tail_max = o.tail_max_slabs > 0 ? o.tail_max_slabs : (NT <= 2 ? 1024 : 512);
-        auto store_of = [&](int l0) {
+        auto store_of = [&](int l0) {  // per level u, f and the pre-smoothed iterate
             long long e = 0;
-            for (int l = l0; l < nl; ++l) e += 2 * n[l] * NT;
+            for (int l = l0; l < nl; ++l) e += 3 * n[l] * NT;
             return e + (e & 1);
         };
         auto smem_of = [&](int l0) {
@@ -560,7 +610,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         for (int l = tl; l < nl; ++l) {
             targ.n[l] = n[l];
             targ.off[l] = off;
-            off += 2 * n[l] * NT;
+            off += 3 * n[l] * NT;
         }
         targ.store_elems = store_elems;
         targ.gstore = gstore;
@@ -575,8 +625,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                                            "(at most %lld slabs here)", tail_max);
         targ.trace = nullptr;
         if (getenv("TMG_TAIL_TRACE")) {
-            CK(cudaMalloc(&d_trace, sizeof(unsigned long long) * 6 * MAXLEV));
-            CK(cudaMemset(d_trace, 0, sizeof(unsigned long long) * 6 * MAXLEV));
+            CK(cudaMalloc(&d_trace, sizeof(unsigned long long) * 10 * MAXLEV));
+            CK(cudaMemset(d_trace, 0, sizeof(unsigned long long) * 10 * MAXLEV));
             targ.trace = d_trace;
         }
         // coarsest solve: serial forward substitution (bitwise) unless asked

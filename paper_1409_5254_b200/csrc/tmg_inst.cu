@@ -2,8 +2,8 @@
 //   -DTMG_T=double|float -DTMG_NT=1..4 -DTMG_PART=0..3
 // The instantiations of a pair are split over four translation units so the
 // build runs them in parallel:
-//   part 0  the dispatcher, generic (runtime-flag) passes, down passes, tail,
-//           coarse solves
+//   part 0  the dispatcher, generic (runtime-flag) passes, down passes
+// (the single-CTA tail engine and the coarse solves: tmg_inst_tail.cu)
 //   part 1  up passes with separately stored pre-sweeps (K_UP, K_UPNORM) and
 //           K_UP2NORM
 //   part 2  the recomputing up passes (K_UP2, K_UP2DOWN)
@@ -11,7 +11,6 @@
 #define TMG_INST_UNIT 1
 #include "tmg_launch.cuh"
 #include "tmg_stream.cuh"
-#include "tmg_tail.cuh"
 
 #ifndef TMG_T
 #error "define TMG_T and TMG_NT"
@@ -145,6 +144,10 @@ int stream_launch(const LevelC<T, NT> &L, const StreamArgs<T> &a, int nu, int ki
 }
 
 template <typename T, int NT> size_t stream_smem_bytes() { return RowLayout<T, NT, true, true>::SMEM_BYTES; }
+
+template int stream_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
+                                          int, bool, cudaStream_t);
+template size_t stream_smem_bytes<TMG_T, TMG_NT>();
 #endif
 
 namespace {
@@ -254,51 +257,6 @@ int stream_v_launch(const LevelC<T, NT> &L0, const LevelC<T, NT> &L1, const Stre
 
 #endif  // part 3
 
-#if TMG_IN_PART(0)
-template <typename T, int NT> int tail_prepare(bool sparse, size_t smem)
-{
-    cudaError_t e = sparse ? cudaFuncSetAttribute(tail_kernel<T, NT, true>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                           : cudaFuncSetAttribute(tail_kernel<T, NT, false>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return (int)e;
-}
-
-template <typename T, int NT>
-int tail_launch(const TailArgs<T, NT> &t, bool sparse, unsigned grid, size_t smem, cudaStream_t s)
-{
-    if (sparse) return (int)launch_pdl(tail_kernel<T, NT, true>, dim3(grid), dim3(TAIL_THREADS), smem, s, t);
-    return (int)launch_pdl(tail_kernel<T, NT, false>, dim3(grid), dim3(TAIL_THREADS), smem, s, t);
-}
-
-template <typename T, int NT>
-int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, long long n, int batch,
-                         int variant, const int *active, cudaStream_t s)
-{
-    const unsigned grid = (unsigned)((batch + 31) / 32);
-    if (sparse) coarse_serial_kernel<T, NT, true><<<grid, 32, 0, s>>>(L, f, u, n, batch, variant, active);
-    else coarse_serial_kernel<T, NT, false><<<grid, 32, 0, s>>>(L, f, u, n, batch, variant, active);
-    return (int)cudaGetLastError();
-}
-
-template <typename T, int NT>
-int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, int batch, const int *active,
-                       cudaStream_t s)
-{
-    coarse_scan_kernel<T, NT><<<(unsigned)batch, 1024, 0, s>>>(L, f, u, n, batch, active);
-    return (int)cudaGetLastError();
-}
-
-template int coarse_scan_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const TMG_T *, TMG_T *, long long,
-                                               int, const int *, cudaStream_t);
-template int stream_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const StreamArgs<TMG_T> &, int, int,
-                                          int, bool, cudaStream_t);
-template size_t stream_smem_bytes<TMG_T, TMG_NT>();
-template int tail_prepare<TMG_T, TMG_NT>(bool, size_t);
-template int tail_launch<TMG_T, TMG_NT>(const TailArgs<TMG_T, TMG_NT> &, bool, unsigned, size_t, cudaStream_t);
-template int coarse_serial_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, bool, const TMG_T *, TMG_T *,
-                                                 long long, int, int, const int *, cudaStream_t);
-#endif  // part 0
 
 #if TMG_IN_PART(3)
 template int stream_d_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const LevelC<TMG_T, TMG_NT> &,

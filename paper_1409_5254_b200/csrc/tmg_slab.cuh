@@ -126,6 +126,7 @@ template <typename T, int NT> struct LevelC {
     T ce[NT];
     T cw[NT];
     T calpha;
+    double calpha_lo;  // alpha - calpha (double-double tail, for the grid-wide scan)
     int scan_ok;
 };
 
@@ -574,6 +575,36 @@ __device__ __forceinline__ void lu_apply_nb(const LevelC<T, NT> &L, T (&y)[NT], 
     }
 }
 
+// a / d, exact, for the fallback of the branch-free LU solves: a zero
+// numerator gives the correctly signed zero a * RN(1/d) (sign(a) xor sign(d),
+// as IEEE division) without the slow division; numerators outside the
+// Markstein window take the IEEE division; the rest the two-correction form
+__device__ __forceinline__ double divq_exact(double a, double d, double rinv)
+{
+    if (a == 0.0) return __dmul_rn(a, rinv);
+    return divq(a, d, rinv);
+}
+__device__ __forceinline__ float divq_exact(float a, float d, float rinv)
+{
+    if (a == 0.0f) return __fmul_rn(a, rinv);
+    return divq(a, d, rinv);
+}
+
+// exact LU solve (the fallback of lu_apply_nb when a numerator left the window)
+template <typename T, int NT> __device__ __forceinline__ void lu_apply_fallback(const LevelC<T, NT> &L, T (&y)[NT])
+{
+#pragma unroll
+    for (int i = 1; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+#pragma unroll
+    for (int i = NT - 1; i >= 0; --i) {
+#pragma unroll
+        for (int j = i + 1; j < NT; ++j) y[i] = FP<T>::sub(y[i], FP<T>::mul(L.lu[i * NT + j], y[j]));
+        y[i] = divq_exact(y[i], L.lu[i * NT + i], L.rinv[i]);
+    }
+}
+
 // exact-IEEE LU solve (the rare fallback of lu_apply_nb)
 template <typename T, int NT> __device__ __forceinline__ void lu_apply_ieee(const LevelC<T, NT> &L, T (&y)[NT])
 {
@@ -618,7 +649,7 @@ __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], 
         for (int q = 0; q < J; ++q) {
 #pragma unroll
             for (int i = 0; i < NT; ++i) y[q][i] = ys[q][i];
-            lu_apply_ieee<T, NT>(L, y[q]);
+            lu_apply_fallback<T, NT>(L, y[q]);
         }
     }
 #pragma unroll
@@ -808,7 +839,7 @@ __device__ __forceinline__ void sweep(const LevelC<T, NT> &L, T (&u)[NT], const 
     if (__builtin_expect(bad != 0, 0)) {
 #pragma unroll
         for (int i = 0; i < NT; ++i) y[i] = ys[i];
-        lu_apply_ieee<T, NT>(L, y);
+        lu_apply_fallback<T, NT>(L, y);
     }
 #pragma unroll
     for (int i = 0; i < NT; ++i) u[i] = FP<T>::add(FP<T>::mul(y[i], L.omega), u[i]);

@@ -407,22 +407,14 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
             bool nz = false;
 #pragma unroll
             for (int q = 0; q < P; ++q) nz |= neg_zero_rows<T, NT>(f[q]);
+            // (inlined: an out-of-line exact path would take the row arrays
+            // by reference and force them into local memory -- 3x slower)
             if (__any_sync(0xffffffffu, nz)) {
-                row_exact<INTERIOR>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
+                row_impl<INTERIOR, true>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
                 return;
             }
         }
         row_impl<INTERIOR, false>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
-    }
-
-    // the rare rows with -0 in f (signed zeros tracked): one out-of-line copy
-    // per kernel instead of one per call site (compile time)
-    template <bool INTERIOR>
-    __device__ __noinline__ void row_exact(T (&u)[P][NT], const T (&f)[P][NT], const T (&uc)[NT],
-                                           long long slab0, long long row_idx, bool warm, int b, T *uo,
-                                           T *fco, bool zg)
-    {
-        row_impl<INTERIOR, true>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
     }
 
     template <bool INTERIOR, bool SZ>

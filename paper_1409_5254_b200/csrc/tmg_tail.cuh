@@ -139,24 +139,36 @@ __global__ void __launch_bounds__(1024)
 extern __shared__ __align__(128) unsigned char tmg_tail_smem[];
 
 constexpr int WARP_MAX = 64;  // levels this small run in warp 0 only (no block barriers)
+constexpr int TAIL_MAXNU = 4;
 
 // Shared-memory layout (byte offsets from tmg_tail_smem):
-//   LevelC[nlev] | int meta[3*nlev] (u offset, f offset, n) | T xv[2][TT][NT]
-//   | unsigned xm[2][TT] | double part[TT] | level store (when SMEM)
+//   LevelC[nlev] | int meta[4*nlev] (u, f, p offsets, n) | T scan scratch[2][TT]
+//   | double part[TT] | level store (when SMEM): per level u, f, p (n*NT each)
+//   | sq[n_l0] (full mode)
+//
+// Per level three arrays: f (right-hand side), p (the iterate after the
+// pre-sweeps) and u (the level's result: iterate or coarse correction).  A
+// level pass reads one set and writes another, so a pass needs ONE barrier
+// and no halo publication: a thread re-derives the few slabs left of its
+// chunk that its chunk depends on (Jacobi couples slab n to n-1 only; after
+// k sweeps from a slab without its predecessor, every slab >= k further is
+// exact), with the level constants in registers:
+//   down(l):  nu1 sweeps (from zero, or from u) + residual + restriction ->
+//             f(l+1), p(l) (+ the norm leaves of the INPUT's residual at l0)
+//   up(l):    u(l) = S^nu2 (p(l) + P u(l+1))
+// Levels of <= WARP_MAX slabs run in warp 0 with warp barriers only.
 template <typename T, int NT, bool SPARSE, bool SMEM> struct Engine {
     using C = Cpl<T, NT, SPARSE>;
     int l0;            // first (finest) level handled here
-    uint32_t o_meta, o_xv, o_xm, o_part, o_store;
+    uint32_t o_meta, o_scan, o_part, o_store;
     T *gbase;          // level store in global memory (!SMEM)
-    double *sq;        // per-slab squares for the norm
-    int xp = 0;        // halo buffer currently valid
-    int nthr;          // participating threads: blockDim.x, or 32 in warp mode (a power of two)
-    int lgthr;         // log2(nthr)
+    double *sq;        // per-slab squared residual norms of level l0 (full mode)
     int scan = 0;      // coarsest solve: 0 = serial forward substitution (bitwise), 1 = scan
+    bool prev_warp = false;  // the previous pass ran in warp mode
     unsigned long long *trace = nullptr;  // [phase kind][level] cycle totals (thread 0 of block 0)
     long long t_mark = 0;
 
-    // phase kinds for the trace: 0 sweep, 1 restrict, 2 prolong, 3 coarse, 4 norm, 5 warp handoff
+    // phase kinds for the trace: 0 down, 2 up, 3 coarse, 4 norm
     __device__ __forceinline__ void tick(int kind, int l)
     {
         if (trace && threadIdx.x == 0) {
@@ -179,57 +191,38 @@ template <typename T, int NT, bool SPARSE, bool SMEM> struct Engine {
         if constexpr (SMEM) return reinterpret_cast<T *>(tmg_tail_smem + o_store) + off;
         else return gbase + off;
     }
-    __device__ __forceinline__ T *U(int l) const { return arr(meta()[3 * (l - l0)]); }
-    __device__ __forceinline__ T *F(int l) const { return arr(meta()[3 * (l - l0) + 1]); }
-    __device__ __forceinline__ int N(int l) const { return meta()[3 * (l - l0) + 2]; }
-    __device__ __forceinline__ T *xv(int w, int t) const
-    {
-        return reinterpret_cast<T *>(tmg_tail_smem + o_xv) + ((size_t)w * blockDim.x + t) * NT;
-    }
-    __device__ __forceinline__ unsigned *xm(int w, int t) const
-    {
-        return reinterpret_cast<unsigned *>(tmg_tail_smem + o_xm) + (size_t)w * blockDim.x + t;
-    }
+    __device__ __forceinline__ T *U(int l) const { return arr(meta()[4 * (l - l0)]); }
+    __device__ __forceinline__ T *F(int l) const { return arr(meta()[4 * (l - l0) + 1]); }
+    __device__ __forceinline__ T *Pre(int l) const { return arr(meta()[4 * (l - l0) + 2]); }
+    __device__ __forceinline__ int N(int l) const { return meta()[4 * (l - l0) + 3]; }
     __device__ __forceinline__ double *part() const
     {
         return reinterpret_cast<double *>(tmg_tail_smem + o_part);
     }
-    __device__ __forceinline__ void sync() const { group_sync(nthr); }
 
-    // contiguous, even-length chunk of the participating thread
-    __device__ __forceinline__ void chunk(int nn, int &a, int &e) const
+    // contiguous, even-length chunk of this thread at a level of n slabs
+    __device__ __forceinline__ void chunk(int n, int &a, int &e) const
     {
-        int m = (nn + nthr - 1) >> lgthr;
+        const int tt = (int)blockDim.x;
+        int m = (n + tt - 1) / tt;
         m += m & 1;
-        a = min(nn, (int)threadIdx.x * m);
-        e = min(nn, a + m);
+        a = min(n, (int)threadIdx.x * m);
+        e = min(n, a + m);
     }
-    // Halo exchange.  Invariant: before a phase that needs level l's halo,
-    // buffer xp holds, per thread, the coupling data of the CURRENT last slab
-    // of its chunk at level l.  Each phase that changes a level publishes its
-    // own last slab into the other buffer and flips xp, so the barrier ending
-    // the phase also publishes the halo: one barrier per sweep.
-    __device__ __forceinline__ void put(const C &c, int w) const
+    __device__ __forceinline__ static bool warp_level(int n) { return n <= WARP_MAX; }
+    // entering a pass: block passes after warp-0 passes need a block barrier
+    // first; in warp mode the other warps skip the pass
+    __device__ __forceinline__ bool enter(int n)
     {
-        if constexpr (SPARSE) {
-            xv(w, threadIdx.x)[0] = c.s;
-            *xm(w, threadIdx.x) = c.m;
-        } else {
-#pragma unroll
-            for (int j = 0; j < NT; ++j) xv(w, threadIdx.x)[j] = c.u[j];
-        }
+        const bool w = warp_level(n);
+        if (!w && prev_warp) __syncthreads();
+        prev_warp = w;
+        return !w || threadIdx.x < 32;
     }
-    __device__ __forceinline__ C get(int t) const
+    __device__ __forceinline__ void leave(int n) const
     {
-        C c;
-        if constexpr (SPARSE) {
-            c.s = xv(xp, t)[0];
-            c.m = *xm(xp, t);
-        } else {
-#pragma unroll
-            for (int j = 0; j < NT; ++j) c.u[j] = xv(xp, t)[j];
-        }
-        return c;
+        if (warp_level(n)) __syncwarp();
+        else __syncthreads();
     }
     __device__ __forceinline__ void load(const T *p, T (&x)[NT]) const
     {
@@ -242,220 +235,347 @@ template <typename T, int NT, bool SPARSE, bool SMEM> struct Engine {
         for (int j = 0; j < NT; ++j) p[j] = x[j];
     }
 
-    __device__ void publish_last(int l)
+    // one damped sweep of two consecutive slabs (two dependency chains): the
+    // pair's old values couple the second to the first; pin = the old value
+    // of the slab before the pair.  Exact IEEE divisions when a numerator
+    // leaves the Markstein window (per thread: no warp vote, chunks differ)
+    __device__ __forceinline__ void sweep2(const LevelC<T, NT> &L, T (&x0)[NT], T (&x1)[NT], const T (&f0)[NT],
+                                           const T (&f1)[NT], const C &pin, bool hp0, C &o1) const
     {
-        int a, e;
-        chunk(N(l), a, e);
-        if (a < e) {
-            T x[NT];
-            load(U(l) + (e - 1) * NT, x);
-            put(make_cpl<T, NT, SPARSE>(Lv(l), x), xp);
+        const C o0 = make_cpl<T, NT, SPARSE>(L, x0);
+        o1 = make_cpl<T, NT, SPARSE>(L, x1);
+        sweep<T, NT, SPARSE>(L, x0, f0, pin, hp0);
+        sweep<T, NT, SPARSE>(L, x1, f1, o0, true);
+    }
+    // the first sweep from the zero guess: u = (omega LU^-1 f) + 0 (bitwise
+    // the full sweep, see sweep_zero_j)
+    __device__ __forceinline__ void sweep_zero1(const LevelC<T, NT> &L, T (&x)[NT], const T (&f)[NT]) const
+    {
+        T u[1][NT], ff[1][NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) ff[0][i] = f[i];
+        if constexpr (fast_fp<T>()) {
+            sweep_zero_j<T, NT, P_GEN, 1>(L, u, ff);
+        } else {
+            // per-thread IEEE fallback (sweep_zero_j votes over the warp)
+            T y[NT], ys[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                T v = f[0];
+#pragma unroll
+                for (int c = 1; c < NT; ++c) v = (L.perm[i] == c) ? f[c] : v;
+                y[i] = v;
+                ys[i] = v;
+            }
+            unsigned bad = 0;
+            lu_apply_nb<T, NT>(L, y, bad);
+            if (__builtin_expect(bad != 0, 0)) {
+#pragma unroll
+                for (int i = 0; i < NT; ++i) y[i] = ys[i];
+                lu_apply_fallback<T, NT>(L, y);
+            }
+#pragma unroll
+            for (int i = 0; i < NT; ++i) u[0][i] = FP<T>::add(FP<T>::mul(y[i], L.omega), T(0));
         }
-        sync();
+#pragma unroll
+        for (int i = 0; i < NT; ++i) x[i] = u[0][i];
     }
 
-    __device__ void sweep_level(int l)
+    // Levels of <= 64 slabs: warp 0, lane t owns the slab pair (2t, 2t+1);
+    // the predecessor of a lane's first slab comes from lane t-1 by a
+    // shuffle (no re-derived halo).  Lanes past the level compute on zeros
+    // and store nothing; every lane takes part in the shuffles.
+    __device__ void down_warp(int l, int n, bool zg, int nu, bool norm)
     {
-        int a, e;
-        chunk(N(l), a, e);
-        if (a < e) {
-            const LevelC<T, NT> &L = Lv(l);
-            T *u = U(l);
-            const T *f = F(l);
-            C prev;
-            cpl_zero(prev);
-            if (a > 0) prev = get(threadIdx.x - 1);
-            T last[NT];
-            int k = a;
-            // slab pairs: two independent dependency chains per thread
-            for (; k + 1 < e; k += 2) {
-                T x0[NT], x1[NT], f0[NT], f1[NT];
-                load(u + k * NT, x0);
-                load(u + (k + 1) * NT, x1);
-                load(f + k * NT, f0);
-                load(f + (k + 1) * NT, f1);
-                C o0 = make_cpl<T, NT, SPARSE>(L, x0);
-                C o1 = make_cpl<T, NT, SPARSE>(L, x1);
-                sweep<T, NT, SPARSE>(L, x0, f0, prev, k > 0);
-                sweep<T, NT, SPARSE>(L, x1, f1, o0, true);
-                store(u + k * NT, x0);
-                store(u + (k + 1) * NT, x1);
-#pragma unroll
-                for (int j = 0; j < NT; ++j) last[j] = x1[j];
-                prev = o1;
+        const int lane = threadIdx.x;
+        const bool act = 2 * lane < n;
+        const LevelC<T, NT> &L = Lv(l);
+        const int j = 2 * lane;
+        T x0[NT], x1[NT], f0[NT], f1[NT];
+        zero_slab<T, NT>(x0);
+        zero_slab<T, NT>(x1);
+        zero_slab<T, NT>(f0);
+        zero_slab<T, NT>(f1);
+        if (act) {
+            load(F(l) + j * NT, f0);
+            load(F(l) + (j + 1) * NT, f1);
+            if (!zg) {
+                load(U(l) + j * NT, x0);
+                load(U(l) + (j + 1) * NT, x1);
             }
-            if (k < e) {
-                T x[NT], ff[NT];
-                load(u + k * NT, x);
-                load(f + k * NT, ff);
-                sweep<T, NT, SPARSE>(L, x, ff, prev, k > 0);
-                store(u + k * NT, x);
-#pragma unroll
-                for (int j = 0; j < NT; ++j) last[j] = x[j];
-            }
-            put(make_cpl<T, NT, SPARSE>(L, last), xp ^ 1);
         }
-        xp ^= 1;
-        sync();
+        const bool hp = lane > 0;
+#pragma unroll
+        for (int k = 0; k < TAIL_MAXNU; ++k) {
+            if (k >= nu) break;
+            if (k == 0 && zg) {
+                if (act) {
+                    sweep_zero1(L, x0, f0);
+                    sweep_zero1(L, x1, f1);
+                }
+                continue;
+            }
+            const C o0 = make_cpl<T, NT, SPARSE>(L, x0);
+            const C pin = cpl_shfl_up<T, NT, SPARSE>(make_cpl<T, NT, SPARSE>(L, x1));
+            if (act) {
+                if (k == 0 && norm) {
+                    T r0[NT], r1[NT];
+                    residual<T, NT, SPARSE>(L, x0, f0, pin, hp, r0);
+                    residual<T, NT, SPARSE>(L, x1, f1, o0, true, r1);
+                    sq[j] = (double)sqnorm<T, NT>(r0);
+                    sq[j + 1] = (double)sqnorm<T, NT>(r1);
+                }
+                sweep<T, NT, SPARSE>(L, x0, f0, pin, hp);
+                sweep<T, NT, SPARSE>(L, x1, f1, o0, true);
+            }
+        }
+        T r0[NT], r1[NT];
+        const C o0 = make_cpl<T, NT, SPARSE>(L, x0);
+        const C pin = cpl_shfl_up<T, NT, SPARSE>(make_cpl<T, NT, SPARSE>(L, x1));
+        residual<T, NT, SPARSE>(L, x0, f0, pin, hp, r0);
+        residual<T, NT, SPARSE>(L, x1, f1, o0, true, r1);
+        if (act) {
+            if (norm && nu == 0) {
+                sq[j] = (double)sqnorm<T, NT>(r0);
+                sq[j + 1] = (double)sqnorm<T, NT>(r1);
+            }
+            store(Pre(l) + j * NT, x0);
+            store(Pre(l) + (j + 1) * NT, x1);
+            T p0[NT], p1[NT];
+            restrict_part<T, NT>(L, r0, false, p0);
+            restrict_part<T, NT>(L, r1, true, p1);
+            T *fc = F(l + 1);
+#pragma unroll
+            for (int i = 0; i < NT; ++i) fc[lane * NT + i] = FP<T>::add(p0[i], p1[i]);
+        }
+        __syncwarp();
+    }
+
+    __device__ void up_warp(int l, int n, int nu)
+    {
+        const int lane = threadIdx.x;
+        const bool act = 2 * lane < n;
+        const LevelC<T, NT> &L = Lv(l);
+        const int j = 2 * lane;
+        T x0[NT], x1[NT], f0[NT], f1[NT];
+        zero_slab<T, NT>(x0);
+        zero_slab<T, NT>(x1);
+        zero_slab<T, NT>(f0);
+        zero_slab<T, NT>(f1);
+        if (act) {
+            T c[NT];
+            load(Pre(l) + j * NT, x0);
+            load(Pre(l) + (j + 1) * NT, x1);
+            load(U(l + 1) + lane * NT, c);
+            prolong_part<T, NT>(L, c, false, x0);
+            prolong_part<T, NT>(L, c, true, x1);
+            if (nu > 0) {
+                load(F(l) + j * NT, f0);
+                load(F(l) + (j + 1) * NT, f1);
+            }
+        }
+        const bool hp = lane > 0;
+#pragma unroll
+        for (int k = 0; k < TAIL_MAXNU; ++k) {
+            if (k >= nu) break;
+            const C o0 = make_cpl<T, NT, SPARSE>(L, x0);
+            const C pin = cpl_shfl_up<T, NT, SPARSE>(make_cpl<T, NT, SPARSE>(L, x1));
+            if (act) {
+                sweep<T, NT, SPARSE>(L, x0, f0, pin, hp);
+                sweep<T, NT, SPARSE>(L, x1, f1, o0, true);
+            }
+        }
+        if (act) {
+            store(U(l) + j * NT, x0);
+            store(U(l) + (j + 1) * NT, x1);
+        }
+        __syncwarp();
+    }
+
+    // down pass of level l (multigrid.py:274-285): nu sweeps from the zero
+    // guess (zg) or from U(l), the residual, the restriction into F(l+1); the
+    // pre-smoothed iterate into Pre(l).  norm: the per-slab squared residual
+    // norms of the INPUT iterate (its first sweep's residual; norm_at,
+    // :447-459) into sq.
+    __device__ void down(int l, bool zg, int nu, bool norm)
+    {
+        const int n = N(l);
+        if (warp_level(n)) {
+            if (enter(n)) down_warp(l, n, zg, nu, norm);
+            tick(0, l);
+            return;
+        }
+        if (enter(n)) {
+            int a, e;
+            chunk(n, a, e);
+            if (a < e) {
+                const LevelC<T, NT> &L = Lv(l);
+                const int hs = max(0, a - (nu + 1)) & ~1;
+                const T *f = F(l), *u = U(l);
+                T *pre = Pre(l), *fc = F(l + 1);
+                C cin[TAIL_MAXNU], cres;  // predecessor data per sweep / for the residual
+#pragma unroll
+                for (int k = 0; k < TAIL_MAXNU; ++k) cpl_zero(cin[k]);
+                cpl_zero(cres);
+                for (int j = hs; j < e; j += 2) {
+                    T x0[NT], x1[NT], f0[NT], f1[NT];
+                    load(f + j * NT, f0);
+                    load(f + (j + 1) * NT, f1);
+                    if (zg) {
+                        zero_slab<T, NT>(x0);
+                        zero_slab<T, NT>(x1);
+                    } else {
+                        load(u + j * NT, x0);
+                        load(u + (j + 1) * NT, x1);
+                    }
+                    const bool hp = j > 0;
+#pragma unroll
+                    for (int k = 0; k < TAIL_MAXNU; ++k) {
+                        if (k >= nu) break;
+                        if (k == 0 && zg) {
+                            sweep_zero1(L, x0, f0);
+                            sweep_zero1(L, x1, f1);
+                            continue;
+                        }
+                        if (k == 0 && norm && j >= a) {
+                            T r0[NT], r1[NT];
+                            const C o0 = make_cpl<T, NT, SPARSE>(L, x0);
+                            residual<T, NT, SPARSE>(L, x0, f0, cin[0], hp, r0);
+                            residual<T, NT, SPARSE>(L, x1, f1, o0, true, r1);
+                            sq[j] = (double)sqnorm<T, NT>(r0);
+                            sq[j + 1] = (double)sqnorm<T, NT>(r1);
+                        }
+                        C o1;
+                        sweep2(L, x0, x1, f0, f1, cin[k], hp, o1);
+                        cin[k] = o1;
+                    }
+                    T r0[NT], r1[NT];
+                    const C o0 = make_cpl<T, NT, SPARSE>(L, x0);
+                    residual<T, NT, SPARSE>(L, x0, f0, cres, hp, r0);
+                    residual<T, NT, SPARSE>(L, x1, f1, o0, true, r1);
+                    cres = make_cpl<T, NT, SPARSE>(L, x1);
+                    if (j >= a) {
+                        if (norm && nu == 0) {
+                            sq[j] = (double)sqnorm<T, NT>(r0);
+                            sq[j + 1] = (double)sqnorm<T, NT>(r1);
+                        }
+                        store(pre + j * NT, x0);
+                        store(pre + (j + 1) * NT, x1);
+                        T p0[NT], p1[NT];
+                        restrict_part<T, NT>(L, r0, false, p0);
+                        restrict_part<T, NT>(L, r1, true, p1);
+#pragma unroll
+                        for (int i = 0; i < NT; ++i) fc[(j >> 1) * NT + i] = FP<T>::add(p0[i], p1[i]);
+                    }
+                }
+            }
+            leave(n);
+        }
         tick(0, l);
     }
 
-    // residual + restriction into level l+1 (multigrid.py:283-285) and the
-    // zero initial guess there (:312)
-    __device__ void restrict_level(int l)
+    // up pass of level l (multigrid.py:317-327): u(l) = S^nu (Pre(l) + P u(l+1))
+    __device__ void up(int l, int nu)
     {
-        int a, e;
-        chunk(N(l), a, e);
-        const LevelC<T, NT> &L = Lv(l);
-        const int nc = N(l) >> 1;
-        const T *u = U(l), *f = F(l);
-        T *fc = F(l + 1), *uc = U(l + 1);
-        if (a < e) {
-            C prev;
-            cpl_zero(prev);
-            if (a > 0) prev = get(threadIdx.x - 1);
-            for (int c = a >> 1; c < (e >> 1) && c < nc; ++c) {
-                T x0[NT], x1[NT], f0[NT], f1[NT], r0[NT], r1[NT], p0[NT], p1[NT];
-                load(u + (2 * c) * NT, x0);
-                load(u + (2 * c + 1) * NT, x1);
-                load(f + (2 * c) * NT, f0);
-                load(f + (2 * c + 1) * NT, f1);
-                residual<T, NT, SPARSE>(L, x0, f0, prev, 2 * c > 0, r0);
-                C c0 = make_cpl<T, NT, SPARSE>(L, x0);
-                residual<T, NT, SPARSE>(L, x1, f1, c0, true, r1);
-                prev = make_cpl<T, NT, SPARSE>(L, x1);
-                restrict_part<T, NT>(L, r0, false, p0);
-                restrict_part<T, NT>(L, r1, true, p1);
+        const int n = N(l);
+        if (warp_level(n)) {
+            if (enter(n)) up_warp(l, n, nu);
+            tick(2, l);
+            return;
+        }
+        if (enter(n)) {
+            int a, e;
+            chunk(n, a, e);
+            if (a < e) {
+                const LevelC<T, NT> &L = Lv(l);
+                const int hs = max(0, a - nu) & ~1;
+                const T *f = F(l), *pre = Pre(l), *uc = U(l + 1);
+                T *u = U(l);
+                C cin[TAIL_MAXNU];
 #pragma unroll
-                for (int i = 0; i < NT; ++i) {
-                    fc[c * NT + i] = FP<T>::add(p0[i], p1[i]);
-                    uc[c * NT + i] = T(0);
+                for (int k = 0; k < TAIL_MAXNU; ++k) cpl_zero(cin[k]);
+                for (int j = hs; j < e; j += 2) {
+                    T x0[NT], x1[NT], f0[NT], f1[NT], c[NT];
+                    load(pre + j * NT, x0);
+                    load(pre + (j + 1) * NT, x1);
+                    load(uc + (j >> 1) * NT, c);
+                    prolong_part<T, NT>(L, c, false, x0);
+                    prolong_part<T, NT>(L, c, true, x1);
+                    if (nu > 0) {
+                        load(f + j * NT, f0);
+                        load(f + (j + 1) * NT, f1);
+                    }
+                    const bool hp = j > 0;
+#pragma unroll
+                    for (int k = 0; k < TAIL_MAXNU; ++k) {
+                        if (k >= nu) break;
+                        C o1;
+                        sweep2(L, x0, x1, f0, f1, cin[k], hp, o1);
+                        cin[k] = o1;
+                    }
+                    if (j >= a) {
+                        store(u + j * NT, x0);
+                        store(u + (j + 1) * NT, x1);
+                    }
                 }
             }
+            leave(n);
         }
-        int ac, ec;
-        chunk(N(l + 1), ac, ec);
-        if (ac < ec) {
-            T z[NT];
-            zero_slab<T, NT>(z);
-            put(make_cpl<T, NT, SPARSE>(Lv(l + 1), z), xp ^ 1);
-        }
-        xp ^= 1;
-        sync();
-        tick(1, l);
-    }
-
-    // u_l += P u_{l+1} (multigrid.py:317)
-    __device__ void prolong_level(int l)
-    {
-        int a, e;
-        chunk(N(l), a, e);
-        const LevelC<T, NT> &L = Lv(l);
-        const int nc = N(l) >> 1;
-        T *u = U(l);
-        const T *uc = U(l + 1);
-        for (int c = a >> 1; c < (e >> 1) && c < nc; ++c) {
-            T cc[NT], x0[NT], x1[NT];
-            load(uc + c * NT, cc);
-            load(u + (2 * c) * NT, x0);
-            load(u + (2 * c + 1) * NT, x1);
-            prolong_part<T, NT>(L, cc, false, x0);
-            prolong_part<T, NT>(L, cc, true, x1);
-            store(u + (2 * c) * NT, x0);
-            store(u + (2 * c + 1) * NT, x1);
-        }
-        if (a < e) {
-            T x[NT];
-            load(u + (e - 1) * NT, x);
-            put(make_cpl<T, NT, SPARSE>(L, x), xp ^ 1);
-        }
-        xp ^= 1;
-        sync();
         tick(2, l);
     }
 
     __device__ void coarse_level(int l, int variant)
     {
+        const int n = N(l);
         if (scan) {
-            T *xs = reinterpret_cast<T *>(tmg_tail_smem + o_xv);
-            cta_scan_solve<T, NT>(Lv(l), F(l), U(l), N(l), xs, xs + blockDim.x, nthr);
+            if (prev_warp) __syncthreads();
+            prev_warp = false;
+            T *xs = reinterpret_cast<T *>(tmg_tail_smem + o_scan);
+            cta_scan_solve<T, NT>(Lv(l), F(l), U(l), n, xs, xs + blockDim.x, (int)blockDim.x);
             tick(3, l);
             return;
         }
-        if (threadIdx.x == 0) forward_substitute<T, NT, SPARSE>(Lv(l), F(l), U(l), N(l), variant);
-        sync();
+        if (enter(n)) {
+            if (threadIdx.x == 0) forward_substitute<T, NT, SPARSE>(Lv(l), F(l), U(l), n, variant);
+            leave(n);
+        }
         tick(3, l);
     }
 
-    // gamma-cycle from level l0 (multigrid.py:263-330), iterative.  In block
-    // mode, the coarse-grid correction of the first level with <= WARP_MAX
-    // slabs below it is handed to warp 0 (warp-synchronous, no block barriers).
-    template <bool WARP>
-    __device__ void cycle(int lstart, int last, int nu1, int nu2, int gamma, int variant)
+    // the rest of a gamma-cycle whose down pass at lstart is done
+    // (multigrid.py:263-330; gamma = 2: the W-cycle of the oracle's
+    // tmo_cycle_rec), iterative: cnt[l] = visits of level l+1 so far
+    __device__ void cycle_rest(int lstart, int last, int nu1, int nu2, int gamma, int variant)
     {
         int cnt[MAXLEV];
         int l = lstart;
-        for (int k = 0; k < nu1; ++k) sweep_level(l);
-        restrict_level(l);
         cnt[l] = 0;
         while (true) {
             if (l + 1 == last) {
                 coarse_level(last, variant);
                 cnt[l] = gamma;
-            } else if (!WARP && cnt[l] == 0 && N(l + 1) <= WARP_MAX) {
-                const int xp0 = xp;
-                if (threadIdx.x < 32) {
-                    const int nt0 = nthr, lg0 = lgthr;
-                    nthr = 32;
-                    lgthr = 5;
-                    publish_last(l + 1);
-                    for (int g = 0; g < gamma; ++g) cycle<true>(l + 1, last, nu1, nu2, gamma, variant);
-                    nthr = nt0;
-                    lgthr = lg0;
-                }
-                xp = xp0;  // the next phase (prolong) publishes afresh
-                __syncthreads();
-                tick(5, l + 1);
-                cnt[l] = gamma;
             }
             if (cnt[l] < gamma) {
+                const bool zg = cnt[l] == 0;  // first visit: zero initial guess (:311-312)
                 cnt[l] += 1;
                 l += 1;
-                for (int k = 0; k < nu1; ++k) sweep_level(l);
-                restrict_level(l);
+                down(l, zg, nu1, false);
                 cnt[l] = 0;
                 continue;
             }
-            prolong_level(l);
-            for (int k = 0; k < nu2; ++k) sweep_level(l);
+            up(l, nu2);
             if (l == lstart) break;
             l -= 1;
         }
     }
 
-    // ||f - L u|| at level l with numpy pairwise order (norm_at, :447-462)
-    __device__ double norm(int l) const
+    // ||r|| of level l0's INPUT iterate from sq (written by down(l0, .., norm))
+    __device__ double norm_reduce(int l)
     {
-        int a, e;
-        chunk(N(l), a, e);
-        const LevelC<T, NT> &L = Lv(l);
-        const T *u = U(l), *f = F(l);
-        if (a < e) {
-            C prev;
-            cpl_zero(prev);
-            if (a > 0) prev = get(threadIdx.x - 1);
-            for (int k = a; k < e; ++k) {
-                T x[NT], ff[NT], r[NT];
-                load(u + k * NT, x);
-                load(f + k * NT, ff);
-                residual<T, NT, SPARSE>(L, x, ff, prev, k > 0, r);
-                prev = make_cpl<T, NT, SPARSE>(L, x);
-                sq[k] = (double)sqnorm<T, NT>(r);
-            }
-        }
         __syncthreads();
-        double nrm = __dsqrt_rn(block_pairwise_auto(sq, N(l), part()));
-        const_cast<Engine *>(this)->tick(4, l);
+        prev_warp = false;
+        const double nrm = __dsqrt_rn(block_pairwise_auto(sq, N(l), part()));
+        tick(4, l);
         return nrm;
     }
 };
@@ -470,19 +590,15 @@ __device__ void tail_body(const TailArgs<T, NT> &a)
         reinterpret_cast<uint32_t *>(tmg_tail_smem)[i] = reinterpret_cast<const uint32_t *>(a.levels + (size_t)b * a.levels_stride + a.l0)[i];
     Engine<T, NT, SPARSE, SMEM> E;
     E.l0 = a.l0;
-    E.nthr = blockDim.x;
-    E.lgthr = 31 - __clz((int)blockDim.x);
     E.scan = a.coarse_scan;
     E.trace = blockIdx.x == 0 ? a.trace : nullptr;
     E.t_mark = clock64();
     uint32_t o = (uint32_t)(sizeof(LevelC<T, NT>) * nlev);
     E.o_meta = o;
-    o += (uint32_t)(sizeof(int) * 3 * nlev);
+    o += (uint32_t)(sizeof(int) * 4 * nlev);
     o = (o + 15) & ~15u;
-    E.o_xv = o;
-    o += (uint32_t)(sizeof(T) * 2 * blockDim.x * NT);
-    E.o_xm = o;
-    o += (uint32_t)(sizeof(unsigned) * 2 * blockDim.x);
+    E.o_scan = o;
+    o += (uint32_t)(sizeof(T) * 2 * blockDim.x);
     o = (o + 15) & ~15u;
     E.o_part = o;
     o += (uint32_t)(sizeof(double) * blockDim.x);
@@ -491,9 +607,11 @@ __device__ void tail_body(const TailArgs<T, NT> &a)
     E.gbase = SMEM ? nullptr : a.gstore + (size_t)b * a.store_elems;
     int *meta = reinterpret_cast<int *>(tmg_tail_smem + E.o_meta);
     for (int l = a.l0 + threadIdx.x; l < a.depth; l += blockDim.x) {
-        meta[3 * (l - a.l0)] = (int)a.off[l];
-        meta[3 * (l - a.l0) + 1] = (int)(a.off[l] + a.n[l] * NT);
-        meta[3 * (l - a.l0) + 2] = (int)a.n[l];
+        const int nn = (int)a.n[l];
+        meta[4 * (l - a.l0)] = (int)a.off[l];
+        meta[4 * (l - a.l0) + 1] = (int)(a.off[l] + (long long)nn * NT);
+        meta[4 * (l - a.l0) + 2] = (int)(a.off[l] + 2LL * nn * NT);
+        meta[4 * (l - a.l0) + 3] = nn;
     }
     E.sq = reinterpret_cast<double *>(E.arr((int)a.store_elems));
     __syncthreads();
@@ -507,26 +625,33 @@ __device__ void tail_body(const TailArgs<T, NT> &a)
         u0[i] = a.u_in ? a.u_in[(size_t)b * ne + i] : T(0);
     }
     __syncthreads();
-    E.publish_last(a.l0);
     const int last = a.depth - 1;
 
     if (!a.full) {
         for (int c = 0; c < a.n_cycles; ++c) {
-            if (a.l0 == last) E.coarse_level(last, a.dot_variant);
-            else E.template cycle<false>(a.l0, last, a.nu1, a.nu2, a.gamma, a.dot_variant);
+            if (a.l0 == last) {
+                E.coarse_level(last, a.dot_variant);
+            } else {
+                E.down(a.l0, c == 0 && !a.u_in, a.nu1, false);
+                E.cycle_rest(a.l0, last, a.nu1, a.nu2, a.gamma, a.dot_variant);
+            }
         }
     } else {
-        // _iterate (multigrid.py:476-492) on one problem
+        // _iterate (multigrid.py:476-492) on one problem; the norm of each
+        // iterate comes from the next cycle's down pass (its first sweep's
+        // residual), which is discarded when the stopping test ends the solve
         double *hist = a.hist + (size_t)b * (a.max_iters + 1);
-        double r0 = E.norm(a.l0);
-        double e = __dmul_rn(a.eps, r0);
-        double tol = e > a.floor_[b] ? e : a.floor_[b];
+        E.down(a.l0, false, a.nu1, true);
+        const double r0 = E.norm_reduce(a.l0);
+        const double e = __dmul_rn(a.eps, r0);
+        const double tol = e > a.floor_[b] ? e : a.floor_[b];
         double rk = r0;
         int iters = 0;
         if (threadIdx.x == 0) hist[0] = r0;
         while (rk > tol && iters < a.max_iters) {
-            E.template cycle<false>(a.l0, last, a.nu1, a.nu2, a.gamma, a.dot_variant);
-            rk = E.norm(a.l0);
+            E.cycle_rest(a.l0, last, a.nu1, a.nu2, a.gamma, a.dot_variant);
+            E.down(a.l0, false, a.nu1, true);
+            rk = E.norm_reduce(a.l0);
             iters += 1;
             if (threadIdx.x == 0) hist[iters] = rk;
         }

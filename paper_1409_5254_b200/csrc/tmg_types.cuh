@@ -71,9 +71,9 @@ template <typename T, int NT> struct TailArgs {
 template <typename T, int NT>
 __host__ __device__ constexpr size_t tail_fixed_smem(int nlev)
 {
-    // LevelC[nlev] | meta | halo values [2][TT][NT] | halo masks [2][TT] | part[TT]
-    return sizeof(LevelC<T, NT>) * (size_t)nlev + sizeof(int) * 3 * (size_t)nlev + sizeof(T) * 2 * TAIL_THREADS * NT +
-           sizeof(unsigned) * 2 * TAIL_THREADS + sizeof(double) * TAIL_THREADS + 64;
+    // LevelC[nlev] | meta[4 nlev] | scan scratch [2][TT] | part[TT] (+ alignment)
+    return sizeof(LevelC<T, NT>) * (size_t)nlev + sizeof(int) * 4 * (size_t)nlev + sizeof(T) * 2 * TAIL_THREADS +
+           sizeof(double) * TAIL_THREADS + 64;
 }
 
 }  // namespace tmg

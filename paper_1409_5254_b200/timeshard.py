@@ -146,12 +146,16 @@ class DistComm:
         self.dist.all_gather(bufs, local.contiguous(), group=self.group)
         return torch.cat(bufs)
 
-    def all_gather_float(self, x: float):
+    def all_gather_value(self, x):
+        """Every rank's scalar (a 1-element float64 tensor on this rank's
+        device, or a float), as a list of 1-element tensors -- no host sync
+        for device tensors (NCCL all_gather on the stream)."""
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device=self.device)
+        t = x if torch.is_tensor(x) else torch.tensor([float(x)], dtype=torch.float64)
+        t = t.reshape(1).to(device=self.device, dtype=torch.float64)
         bufs = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(bufs, t, group=self.group)
-        return [float(b.item()) for b in bufs]
+        return bufs
 
 
 # ---------------------------------------------------------------------------
@@ -190,22 +194,28 @@ class CudaSlabOps:
     def download(self, t):
         return t.cpu().numpy()
 
-    def down(self, l, f, u_in, u_out, fc, nu):
+    def active_flag(self):
+        """The device stopping mask the passes honour (int32, 1 = keep going)."""
+        return self.torch.ones(1, dtype=self.torch.int32, device="cuda")
+
+    def down(self, l, f, u_in, u_out, fc, nu, active=None):
         d = self._desc(l, f.shape[0])
         nat.check(self.lib.tmg_down(nat.F64, ctypes.byref(d), self._p(f), self._p(u_in), self._p(u_out),
-                                    self._p(fc), 1, int(nu), None, self._s()), "tmg_down")
+                                    self._p(fc), 1, int(nu), self._p(active), self._s()), "tmg_down")
 
-    def up(self, l, f, u_in, uc, u_out, nu):
+    def up(self, l, f, u_in, uc, u_out, nu, active=None):
         d = self._desc(l, f.shape[0])
         nat.check(self.lib.tmg_up(nat.F64, ctypes.byref(d), self._p(f), self._p(u_in), self._p(uc),
-                                  self._p(u_out), None, 1, int(nu), None, self._s()), "tmg_up")
+                                  self._p(u_out), None, 1, int(nu), self._p(active), self._s()), "tmg_up")
 
     def resid_sqsum(self, f, u, skip):
+        """This rank's numpy-order share of the squared norm: a 1-element
+        device tensor (stream-ordered, no host sync)."""
         d = self._desc(0, f.shape[0])
         out = self.torch.empty(1, dtype=self.torch.float64, device="cuda")
         nat.check(self.lib.tmg_resid_sqsum(nat.F64, ctypes.byref(d), self._p(f), self._p(u), int(skip),
                                            self._p(out), 1, self._s()), "tmg_resid_sqsum")
-        return float(out.item())
+        return out
 
     def tail_cycle(self, level, f_full):
         """V-cycle from ``level`` down with a zero initial guess (every rank
@@ -270,16 +280,16 @@ class TimeShardedSolver:
     def _shift(self, buf):
         self.comm.shift(buf[-self.H:], buf[:self.H])
 
-    def _cycle(self, l):
+    def _cycle(self, l, active=None):
         c, o, H = self.config, self.ops, self.H
         G = self.layout.gather_level
         zero = l > 0
         o.down(l, self._own(self.F[l]), None if zero else self._own(self.U[l]), self._own(self.P[l]),
-               self._coarse_out(self.F[l + 1]), c.nu1)
+               self._coarse_out(self.F[l + 1]), c.nu1, active=active)
         self._shift(self.P[l])
         if l + 1 < G:
             self._shift(self.F[l + 1])
-            self._cycle(l + 1)
+            self._cycle(l + 1, active)
         else:
             m, g = self.layout.local[G], self.comm.rank
             f_full = self.comm.all_gather_rows(self.F[G][H:])
@@ -288,16 +298,28 @@ class TimeShardedSolver:
             if g > 0:
                 self.U[G][:H] = u_full[g * m - H:g * m]
         o.up(l, self._own(self.F[l]), self._own(self.P[l]), self._coarse_out(self.U[l + 1]),
-             self._own(self.U[l]), c.nu2)
+             self._own(self.U[l]), c.nu2, active=active)
         self._shift(self.U[l])
 
     def _norm(self):
+        """||f - L u|| of the whole problem as a 1-element tensor on the
+        comm's device: the ranks' numpy-order partial sums, combined in the
+        recursion's own tree (bitwise the single-device np.sum), IEEE sqrt --
+        all on the device, no host sync."""
+        import torch
         skip = 0 if self.comm.rank == 0 else self.H
         s = self.ops.resid_sqsum(self._own(self.F[0]), self._own(self.U[0]), skip)
-        return math.sqrt(combine_pairwise(self.comm.all_gather_float(s)))
+        return torch.sqrt(combine_pairwise(self.comm.all_gather_value(s)))
 
-    def solve(self, f, u_init=None):
-        """(u, SolveStats) with the stopping rule of _iterate (multigrid.py:427-500)."""
+    def solve(self, f, u_init=None, check_every: int = 4):
+        """(u, SolveStats) with the stopping rule of _iterate (multigrid.py:427-500).
+
+        The stopping test runs on the device: every cycle updates a device
+        flag active = (r_k > tol) & (k < max_iters) that the level passes
+        honour (a finished solve's remaining queued cycles are no-ops), and the
+        host looks at it once per ``check_every`` cycles -- no host round trip
+        per cycle.  Iterates, norms and counts equal the per-cycle test's."""
+        import torch
         c, H = self.config, self.H
         f = np.ascontiguousarray(f, dtype=np.float64)
         N = self.layout.n[0]
@@ -315,14 +337,29 @@ class TimeShardedSolver:
         floor = 1e-12 * float(np.linalg.norm(f))
         t0 = time.perf_counter()
         r0 = self._norm()
-        norms = [r0]
-        tol = max(c.eps * r0, floor)
-        rk, iters = r0, 0
-        while rk > tol and iters < c.max_iters:
-            self._cycle(0)
-            rk = self._norm()
-            iters += 1
-            norms.append(rk)
+        dev = r0.device
+        tol = torch.maximum(r0 * c.eps, torch.tensor([floor], dtype=torch.float64, device=dev))
+        hist = [r0]
+        iters_t = torch.zeros(1, dtype=torch.int32, device=dev)
+        active = r0 > tol
+        act = self.ops.active_flag() if hasattr(self.ops, "active_flag") else None
+        queued = 0
+        while queued < c.max_iters:
+            for _ in range(max(1, int(check_every))):
+                if queued >= c.max_iters:
+                    break
+                if act is not None:
+                    act.copy_(active.to(act.dtype).to(act.device))
+                self._cycle(0, act if act is not None else active)
+                rk = self._norm()
+                hist.append(rk)
+                iters_t = iters_t + active.to(torch.int32)
+                active = active & (rk > tol) & (iters_t < c.max_iters)
+                queued += 1
+            if not bool(active.item()):
+                break
+        iters = int(iters_t.item())
+        norms = [float(v) for v in torch.cat(hist[:iters + 1]).cpu()]
         u = self.comm.all_gather_rows(self.U[0][H:])
         elapsed = time.perf_counter() - t0
         stats = SolveStats(iterations=iters, residual_norms=norms, factor=max_ratio(norms),

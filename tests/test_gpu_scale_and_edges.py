@@ -318,3 +318,24 @@ def test_rhs_device_callable_and_solve():
     _, st_d = tmg.solve(hier, dev, 0.0, cfg)
     _, st_h = tmg.solve(hier, host, 0.0, cfg)
     assert st_d.iterations == st_h.iterations
+
+
+# --------------------------------------------------------------------------- single-CTA engine
+
+@pytest.mark.parametrize("p_t", [0, 1, 2, 3])
+@pytest.mark.parametrize("n", [4, 8, 16, 64, 512])
+def test_tail_cycle_sparse_forcing(oracle_mod, p_t, n):
+    """One V-cycle of a problem that lives in the single-CTA engine, with
+    zero slabs in f (exact zeros and the IEEE-division fallback of the LU
+    solves): bitwise the oracle's cycle (multigrid.py:263-330)."""
+    nt = p_t + 1
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(p_t), 1.0 / n, n, coarsest=2)
+    rng = np.random.default_rng(n + p_t)
+    f = np.zeros((n, nt))
+    idx = rng.integers(0, n, max(1, n // 8))
+    f[idx] = rng.standard_normal((len(idx), nt))
+    for u0 in (np.zeros_like(f), rng.standard_normal((n, nt))):
+        cfg = tmg.CycleConfig(nu1=1, nu2=2)
+        got = tmg.v_cycle(hier, u0, f, cfg)
+        want = oracle_mod.cycle(hier, omegas(hier), u0, f, 1, 2)
+        assert same_bits(got, want)

@@ -44,14 +44,18 @@ class OracleSlabOps:
     def download(self, t):
         return t.numpy()
 
-    def down(self, l, f, u_in, u_out, fc, nu):
+    def down(self, l, f, u_in, u_out, fc, nu, active=None):
+        if active is not None and not bool(active):
+            return  # the solve has stopped: queued cycles are no-ops
         lev = self.hier.levels[l]
         u = np.zeros(tuple(f.shape)) if u_in is None else u_in.numpy()
         uo, fco = self.O.down_pass(lev.ops, lev.r1, lev.r2, self.om[l], u, f.numpy(), nu)
         u_out[:] = torch.from_numpy(uo)
         fc[:] = torch.from_numpy(fco)
 
-    def up(self, l, f, u_in, uc, u_out, nu):
+    def up(self, l, f, u_in, uc, u_out, nu, active=None):
+        if active is not None and not bool(active):
+            return
         lev = self.hier.levels[l]
         x = self.O.prolong_add(lev.ops, lev.r1, lev.r2, uc.numpy()[: f.shape[0] // 2], u_in.numpy())
         u_out[:] = torch.from_numpy(self.O.block_jacobi(lev.ops, x, f.numpy(), self.om[l], nu))
@@ -79,16 +83,17 @@ def _case(p_t, n, nu, seed=3):
     return hier, rhs, cfg
 
 
-def _gloo_worker(rank, world, port, p_t, n, nu, min_local, out):
+def _gloo_worker(rank, world, port, p_t, n, nu, min_local, out, max_iters=250):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     hier, rhs, cfg = _case(p_t, n, nu)
+    cfg.max_iters = max_iters
     depth = len(hier.levels)
     om = [tmg.optimal_omega(tmg.alpha(hier.basis, l.tau)) for l in hier.levels]
     ops = OracleSlabOps(hier, om, nu, nu, depth)
     s = ts.TimeShardedSolver(hier, cfg, ts.DistComm(), ops, halo=64, min_local=min_local)
-    u, st = s.solve(rhs, np.zeros_like(rhs))
+    u, st = s.solve(rhs, np.zeros_like(rhs), check_every=3)
     out[rank] = (u.tobytes(), st.residual_norms, st.iterations, s.layout.gather_level)
     dist.destroy_process_group()
 
@@ -109,6 +114,23 @@ def test_gloo_time_sharded_solve_bitwise(oracle_mod, world, p_t, n, nu, min_loca
         assert it == iters
         assert nr == norms
         assert ub == ur.tobytes()
+
+
+def test_gloo_time_sharded_max_iters_mid_batch(oracle_mod):
+    """max_iters reached inside a batch of queued cycles: the device flag
+    turns the rest into no-ops; result = the oracle's 3-cycle iterate."""
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_gloo_worker, args=(2, port, 1, 1 << 13, 1, 256, out, 3), nprocs=2, join=True)
+        res = dict(out)
+    hier, rhs, cfg = _case(1, 1 << 13, 1)
+    om = [tmg.optimal_omega(tmg.alpha(hier.basis, l.tau)) for l in hier.levels]
+    ur, norms, iters = oracle_mod.iterate(hier, om, rhs, np.zeros_like(rhs), 1, 1, 1e-8, 3)
+    assert iters == 3
+    for r in range(2):
+        ub, nr, it, _ = res[r]
+        assert it == 3 and nr == norms and ub == ur.tobytes()
 
 
 def test_pairwise_structure():
@@ -164,8 +186,8 @@ class ThreadComm:
     def all_gather_rows(self, local):
         return torch.cat(self._exchange(local.clone()))
 
-    def all_gather_float(self, x):
-        return self._exchange(float(x))
+    def all_gather_value(self, x):
+        return [v.reshape(1) for v in self._exchange(x)]
 
 
 @pytest.mark.gpu

@@ -41,31 +41,29 @@ int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, 
     return (int)cudaGetLastError();
 }
 
-// exact solve by the grid-wide decoupled look-back scan (tmg_scan.cuh): the
-// tile states and the tile counter live in a stream-ordered allocation
+// exact solve by the grid-wide three-pass scan (tmg_scan.cuh): tile maps and
+// carries in a stream-ordered allocation
 template <typename T, int NT>
 int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, int batch, const int *active,
                        cudaStream_t s)
 {
     if (n <= 0 || batch <= 0) return 0;
-    const long long tile = 32LL * scan_groups<NT>();
-    const long long tiles_per = (n + tile - 1) / tile;
-    const size_t st_bytes = sizeof(ScanTileState) * (size_t)tiles_per * batch;
+    const long long tiles_per = (n + ScanTile<T, NT>::SLABS - 1) / ScanTile<T, NT>::SLABS;
+    const size_t maps_bytes = sizeof(ScanTileMap) * (size_t)tiles_per * batch;
+    const size_t carry_bytes = sizeof(ScanCarry) * (size_t)tiles_per * batch;
     void *ws = nullptr;
-    cudaError_t e = cudaMallocAsync(&ws, st_bytes + 16, s);
+    cudaError_t e = cudaMallocAsync(&ws, maps_bytes + carry_bytes, s);
     if (e != cudaSuccess) return (int)e;
-    e = cudaMemsetAsync(ws, 0, st_bytes + 16, s);
-    if (e == cudaSuccess) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const long long warps = tiles_per * batch;
-        const long long ctas = std::min<long long>((warps + SCAN_WARPS - 1) / SCAN_WARPS, (long long)sms * 8);
-        scan_solve_kernel<T, NT><<<(unsigned)ctas, SCAN_WARPS * 32, 0, s>>>(
-            L, f, u, n, batch, tiles_per, reinterpret_cast<ScanTileState *>(ws),
-            reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + st_bytes), active);
-        e = cudaGetLastError();
-    }
+    auto *maps = reinterpret_cast<ScanTileMap *>(ws);
+    auto *carry = reinterpret_cast<ScanCarry *>(static_cast<char *>(ws) + maps_bytes);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned ctas = (unsigned)std::min<long long>(tiles_per * batch, (long long)sms * 4);
+    scan_agg_kernel<T, NT><<<ctas, SCAN_WARPS * 32, 0, s>>>(L, f, n, batch, tiles_per, maps, active);
+    scan_carry_kernel<T, NT><<<(unsigned)batch, SCAN_CARRY_THREADS, 0, s>>>(L, tiles_per, maps, carry, active);
+    scan_replay_kernel<T, NT><<<ctas, SCAN_WARPS * 32, 0, s>>>(L, f, u, n, batch, tiles_per, carry, active);
+    e = cudaGetLastError();
     cudaError_t e2 = cudaFreeAsync(ws, s);
     return (int)(e != cudaSuccess ? e : e2);
 }

@@ -1,25 +1,33 @@
 // Grid-wide exact solve of the block lower-bidiagonal system L u = f as an
-// associative scan with decoupled look-back (forward_solve, dg.py:290-303,
-// and the coarsest-level solve, multigrid.py:200-205, method "scan").
+// associative scan (forward_solve, dg.py:290-303, and the coarsest-level
+// solve, multigrid.py:200-205, method "scan").
 //
 // The sparse coupling N = outer(eval_start, eval_end) is rank one, so with
 // g_k = LU^-1 f_k and h_k = e.g_k the block recurrence collapses to a scalar
 // affine one (LevelC::ce, cw, calpha):
 //     s_k = alpha s_{k-1} + h_k,      u_k = g_k + s_{k-1} w,      s_{-1} = 0.
-// Each warp owns a tile of SCAN_GROUPS x 32 consecutive slabs (a power of two;
-// one slab per lane per group, so every load and store is a coalesced
-// 32-slab row):
-//   1. g, h per slab; warp-inclusive scan of the maps x -> alpha x + h per
-//      group (5 shuffle steps); the tile's map (A, H) by composing the groups;
-//   2. publish (A, H), look back over the preceding tiles of the problem,
-//      32 at a time (aggregates until an inclusive prefix) for the incoming
-//      s, publish the tile's inclusive s;
-//   3. replay: u = g + s_prev w from the registers (f is read once, u
-//      written once: 2 n_t s bytes per slab, HBM-bound).
-// Tiles are handed out in order by an atomic counter, so every tile a warp
-// waits for is already running (no deadlock).  Not bitwise with the serial
-// substitution (different association; |alpha| <= 1 keeps it stable): the
-// result agrees with the extended-precision solution to a few ulp per slab.
+// Three passes, no inter-CTA waiting; a tile is one CTA: SCAN_WARPS warps of
+// SCAN_GROUPS x 32 consecutive slabs (one slab per lane per group, so loads
+// and stores are coalesced 32-slab rows):
+//   1. scan_agg_kernel: g, h per slab; each lane's inclusive sum over its
+//      group  H_l = sum_{i <= l} alpha^(l-i) h_i  by 5 shuffle steps with the
+//      constant multipliers alpha^(2^k); the groups', warps' and tile's maps
+//      x -> A x + H (A = alpha^(slabs)); only the tile's H is written;
+//   2. scan_carry_kernel: one CTA per problem scans the tiles' maps (chunks
+//      per thread, then the CTA) into each tile's incoming s;
+//   3. scan_replay_kernel: every tile again (f re-read, g recomputed), each
+//      warp's incoming s from the tile's and the preceding warps' maps, the
+//      lanes' s_prev, u = g + s_prev w written once.
+// HBM: f twice, u once (3 n_t s bytes per slab against 2 for one pass).
+// The maps are composed in double-double with alpha itself in double-double
+// (LevelC::calpha + calpha_lo, formed on the host): alpha is applied ~N times,
+// so a rounded alpha (or alpha^k) would be a SYSTEMATIC error growing
+// linearly along the recurrence -- for alpha -> 1 (small tau) ~1e-11 relative
+// at 2^20.  In double-double the scan agrees with the extended-precision
+// solution of the same system to a few ulp per slab (tests: scan vs
+// long-double substitution), i.e. it is more accurate than the serial sweep,
+// whose own error grows like sqrt(N) ulp.  Not bitwise with the serial
+// substitution (different association).
 #pragma once
 #include "tmg_slab.cuh"
 
@@ -37,11 +45,11 @@ constexpr int SCAN_WARPS = 8;     // warps per CTA
 // the extended-precision solution of the same system to a few ulp per slab
 // (tests: scan vs long-double substitution), i.e. it is more accurate than
 // the serial sweep, whose own error grows like sqrt(N) ulp.
-struct ScanTileState {
-    double Ahi, Alo, Hhi, Hlo;  // the tile's map x -> A x + H (flag >= 1)
-    double Shi, Slo;            // s after the tile (flag 2)
-    int flag;                   // 0: nothing yet, 1: aggregate, 2: aggregate + inclusive
-    int pad;
+struct ScanTileMap {
+    double Hhi, Hlo;            // the tile's map x -> alpha^(slabs) x + H
+};
+struct ScanCarry {
+    double hi, lo;              // s before the tile
 };
 
 struct DD {
@@ -77,164 +85,203 @@ __device__ __forceinline__ DD dd_mul_add(DD a, DD b, DD c)
 }
 
 
-// spin with relaxed loads (an acquire load per poll would invalidate L1 every
-// iteration); the caller fences once after seeing the flag set
-__device__ __forceinline__ int scan_flag_poll(const int *p)
+template <typename T, int NT> struct ScanTile {
+    static constexpr int GROUPS = scan_groups<NT>();
+    static constexpr long long WARP_SLABS = 32LL * GROUPS;
+    static constexpr long long SLABS = WARP_SLABS * SCAN_WARPS;
+};
+
+// alpha^(2^k), k = 0..log2(SCAN_WARPS * WARP_SLABS): the multipliers of the
+// shuffle scan (k < 5), of a group (k = 5), of a warp and of a tile
+struct ScanPowers {
+    DD p[16];
+};
+__device__ __forceinline__ ScanPowers scan_powers(const DD &alpha, int kmax)
 {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+    ScanPowers P;
+    P.p[0] = alpha;
+    for (int k = 1; k <= kmax && k < 16; ++k) P.p[k] = dd_mul(P.p[k - 1], P.p[k - 1]);
+    return P;
 }
-__device__ __forceinline__ void scan_fence_acquire()
+
+// one warp's slabs: g (registers), the lanes' inclusive sums per group, the
+// warp's H (all lanes); lanes past the end of the problem contribute h = 0
+template <typename T, int NT>
+__device__ __forceinline__ DD scan_warp(const LevelC<T, NT> &L, const ScanPowers &P, const T *fb, long long n,
+                                        long long s0, int lane, T (&g)[ScanTile<T, NT>::GROUPS][NT],
+                                        double (&iH)[ScanTile<T, NT>::GROUPS])
 {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
-__device__ __forceinline__ void scan_flag_store(int *p, int v)
-{
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    constexpr int G = ScanTile<T, NT>::GROUPS;
+    DD WH{0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const long long k = s0 + 32LL * j + lane;
+        T x[NT];
+        if (k < n) {
+            load_slab<T, NT>(fb + k * NT, x);
+        } else {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) x[i] = T(0);
+        }
+        lu_solve<T, NT>(L, x, g[j]);
+        T h = FP<T>::mul(L.ce[0], g[j][0]);
+#pragma unroll
+        for (int i = 1; i < NT; ++i) h = FP<T>::fma(L.ce[i], g[j][i], h);
+        // within a warp in double (its rounding stays local to the warp's
+        // slabs); the tile and carry compositions, which run along the whole
+        // recurrence with the same multiplier, in double-double
+        double H = k < n ? (double)h : 0.0;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int off = 1 << q;
+            const double ph = __shfl_up_sync(0xffffffffu, H, off);
+            if (lane >= off) H = __fma_rn(P.p[q].hi, ph, H);  // H_l += alpha^off H_{l-off}
+        }
+        iH[j] = H;
+        WH.hi = __fma_rn(P.p[5].hi, WH.hi, __shfl_sync(0xffffffffu, H, 31));  // x -> alpha^32 x + H_group
+    }
+    return WH;
 }
 
 template <typename T, int NT>
-__global__ void __launch_bounds__(SCAN_WARPS * 32, 2)
-    scan_solve_kernel(const __grid_constant__ LevelC<T, NT> L, const T *f, T *u, long long n, int batch,
-                      long long tiles_per, ScanTileState *st, unsigned long long *counter, const int *active)
+__global__ void __launch_bounds__(SCAN_WARPS * 32)
+    scan_agg_kernel(const __grid_constant__ LevelC<T, NT> L, const T *f, long long n, int batch,
+                    long long tiles_per, ScanTileMap *maps, const int *active)
 {
-    const int lane = threadIdx.x & 31;
+    constexpr int G = ScanTile<T, NT>::GROUPS;
+    constexpr int LOGW = 31 - __builtin_clz((unsigned)ScanTile<T, NT>::WARP_SLABS);
+    __shared__ double sh[SCAN_WARPS], sl[SCAN_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const ScanPowers P = scan_powers(DD{(double)L.calpha, L.calpha_lo}, LOGW);
     const long long total = tiles_per * batch;
-    constexpr int SCAN_GROUPS = scan_groups<NT>();
-    const long long TILE = 32LL * SCAN_GROUPS;
-    const DD alpha{(double)L.calpha, L.calpha_lo};
-    while (true) {
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(counter, 1ULL);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if ((long long)t >= total) return;
-        const long long b = (long long)t / tiles_per;
-        const long long tile = (long long)t - b * tiles_per;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        const long long b = t / tiles_per, tile = t - b * tiles_per;
         if (active && !active[b]) continue;
-        const T *fb = f + (size_t)b * n * NT;
-        T *ub = u + (size_t)b * n * NT;
-        ScanTileState *sb = st + b * tiles_per;
-        const long long s0 = tile * TILE;
-
-        // 1. per group: g, h; inclusive double-double scan of the maps
-        //    x -> alpha x + h over the lanes (past the end: identity)
-        T g[SCAN_GROUPS][NT];
-        DD iH[SCAN_GROUPS], gA[SCAN_GROUPS];  // per group: lanes' inclusive H, the group's multiplier
-        DD laneA{1.0, 0.0};                   // alpha^(lane+1): a lane's inclusive multiplier
-#pragma unroll
-        for (int j = 0; j < SCAN_GROUPS; ++j) {
-            const long long k = s0 + 32LL * j + lane;
-            T x[NT];
-            if (k < n) {
-                load_slab<T, NT>(fb + k * NT, x);
-            } else {
-#pragma unroll
-                for (int i = 0; i < NT; ++i) x[i] = T(0);
-            }
-            lu_solve<T, NT>(L, x, g[j]);
-            T h = FP<T>::mul(L.ce[0], g[j][0]);
-#pragma unroll
-            for (int i = 1; i < NT; ++i) h = FP<T>::fma(L.ce[i], g[j][i], h);
-            DD A = k < n ? alpha : DD{1.0, 0.0}, H{k < n ? (double)h : 0.0, 0.0};
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const DD pa{__shfl_up_sync(0xffffffffu, A.hi, off), __shfl_up_sync(0xffffffffu, A.lo, off)};
-                const DD ph{__shfl_up_sync(0xffffffffu, H.hi, off), __shfl_up_sync(0xffffffffu, H.lo, off)};
-                if (lane >= off) {
-                    H = dd_mul_add(A, ph, H);  // (A, H) o (pa, ph): x -> A (pa x + ph) + H
-                    A = dd_mul(A, pa);
-                }
-            }
-            if (j == 0) laneA = A;
-            iH[j] = H;
-            gA[j] = DD{__shfl_sync(0xffffffffu, A.hi, 31), __shfl_sync(0xffffffffu, A.lo, 31)};
-        }
-        // the tile's map: the groups' maps composed in order
-        DD TA{1.0, 0.0}, TH{0.0, 0.0};
-#pragma unroll
-        for (int j = 0; j < SCAN_GROUPS; ++j) {
-            const DD gh{__shfl_sync(0xffffffffu, iH[j].hi, 31), __shfl_sync(0xffffffffu, iH[j].lo, 31)};
-            TH = dd_mul_add(gA[j], TH, gh);
-            TA = dd_mul(gA[j], TA);
-        }
-
-        // 2. decoupled look-back for the incoming s (double-double), one
-        //    window of 32 preceding tiles per step (a tile per lane): the
-        //    nearest tile with its inclusive s ends the walk, the aggregates
-        //    before it are composed with a shuffle tree
-        if (lane == 0 && tile > 0) {
-            sb[tile].Ahi = TA.hi;
-            sb[tile].Alo = TA.lo;
-            sb[tile].Hhi = TH.hi;
-            sb[tile].Hlo = TH.lo;
-            scan_flag_store(&sb[tile].flag, 1);
-        }
-        DD accA{1.0, 0.0}, accH{0.0, 0.0};  // s_in = accA * (s after the window) + accH
-        for (long long w0 = tile - 1; w0 >= 0; w0 -= 32) {
-            const long long p = w0 - lane;
-            int fl = 2;
-            DD a{0.0, 0.0}, h{0.0, 0.0};  // before the problem start: s = 0 (a constant map)
-            if (p >= 0) {
-                while ((fl = scan_flag_poll(&sb[p].flag)) == 0) {
-                }
-                scan_fence_acquire();
-                if (fl == 2) {
-                    h = DD{*(volatile double *)&sb[p].Shi, *(volatile double *)&sb[p].Slo};
-                } else {
-                    a = DD{*(volatile double *)&sb[p].Ahi, *(volatile double *)&sb[p].Alo};
-                    h = DD{*(volatile double *)&sb[p].Hhi, *(volatile double *)&sb[p].Hlo};
-                }
-            }
-            const unsigned m2 = __ballot_sync(0xffffffffu, fl == 2);
-            const int k = m2 ? __ffs(m2) - 1 : 32;
-            if (lane > k) {  // beyond the nearest inclusive tile: not needed
-                a = DD{1.0, 0.0};
-                h = DD{0.0, 0.0};
-            }
-            // map_0 o map_1 o ... o map_31 (lane 0 = the nearest tile, applied last)
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const DD pa{__shfl_down_sync(0xffffffffu, a.hi, off), __shfl_down_sync(0xffffffffu, a.lo, off)};
-                const DD ph{__shfl_down_sync(0xffffffffu, h.hi, off), __shfl_down_sync(0xffffffffu, h.lo, off)};
-                if (lane + off < 32) {
-                    h = dd_mul_add(a, ph, h);
-                    a = dd_mul(a, pa);
-                }
-            }
-            accH = dd_mul_add(accA, h, accH);  // meaningful in lane 0
-            accA = dd_mul(accA, a);
-            if (k < 32) break;
-        }
-        DD sin{__shfl_sync(0xffffffffu, accH.hi, 0), __shfl_sync(0xffffffffu, accH.lo, 0)};
+        T g[G][NT];
+        double iH[G];
+        const DD WH = scan_warp<T, NT>(L, P, f + (size_t)b * n * NT, n,
+                                       tile * ScanTile<T, NT>::SLABS + warp * ScanTile<T, NT>::WARP_SLABS, lane,
+                                       g, iH);
         if (lane == 0) {
-            const DD sout = dd_mul_add(TA, sin, TH);
-            sb[tile].Ahi = TA.hi;
-            sb[tile].Alo = TA.lo;
-            sb[tile].Hhi = TH.hi;
-            sb[tile].Hlo = TH.lo;
-            sb[tile].Shi = sout.hi;
-            sb[tile].Slo = sout.lo;
-            scan_flag_store(&sb[tile].flag, 2);
+            sh[warp] = WH.hi;
+            sl[warp] = WH.lo;
         }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            DD TH{0.0, 0.0};
+            for (int w = 0; w < SCAN_WARPS; ++w) TH = dd_mul_add(P.p[LOGW], TH, DD{sh[w], sl[w]});
+            maps[t] = ScanTileMap{TH.hi, TH.lo};
+        }
+        __syncthreads();
+    }
+}
 
-        // 3. replay from the registers: u = g + s_prev w, s_prev in double-double
+// one CTA per problem: each thread composes a contiguous run of tile maps
+// (x -> A x + H_k, A = alpha^tile), the runs are scanned across the CTA,
+// each thread then writes its tiles' incoming s (all in double-double)
+constexpr int SCAN_CARRY_THREADS = 512;
+template <typename T, int NT>
+__global__ void __launch_bounds__(SCAN_CARRY_THREADS)
+    scan_carry_kernel(const __grid_constant__ LevelC<T, NT> L, long long tiles_per, const ScanTileMap *maps,
+                      ScanCarry *carry, const int *active)
+{
+    constexpr int LOGT = 31 - __builtin_clz((unsigned)ScanTile<T, NT>::SLABS);
+    __shared__ double sAh[SCAN_CARRY_THREADS], sAl[SCAN_CARRY_THREADS], sHh[SCAN_CARRY_THREADS],
+        sHl[SCAN_CARRY_THREADS];
+    const int b = blockIdx.x;
+    if (active && !active[b]) return;
+    const ScanPowers P = scan_powers(DD{(double)L.calpha, L.calpha_lo}, LOGT);
+    const DD TA = P.p[LOGT];
+    const int t = threadIdx.x, Pn = blockDim.x;
+    const ScanTileMap *mb = maps + (size_t)b * tiles_per;
+    ScanCarry *cb = carry + (size_t)b * tiles_per;
+    const long long m = (tiles_per + Pn - 1) / Pn;
+    const long long a = min(tiles_per, (long long)t * m), e = min(tiles_per, a + m);
+    DD A{1.0, 0.0}, H{0.0, 0.0};  // the run's map
+    for (long long k = a; k < e; ++k) {
+        const ScanTileMap q = mb[k];
+        H = dd_mul_add(TA, H, DD{q.Hhi, q.Hlo});
+        A = dd_mul(TA, A);
+    }
+    sAh[t] = A.hi;
+    sAl[t] = A.lo;
+    sHh[t] = H.hi;
+    sHl[t] = H.lo;
+    __syncthreads();
+    for (int off = 1; off < Pn; off <<= 1) {  // inclusive scan of the runs' maps
+        DD pa{1.0, 0.0}, ph{0.0, 0.0};
+        if (t >= off) {
+            pa = DD{sAh[t - off], sAl[t - off]};
+            ph = DD{sHh[t - off], sHl[t - off]};
+        }
+        __syncthreads();
+        if (t >= off) {
+            H = dd_mul_add(A, ph, H);
+            A = dd_mul(A, pa);
+            sAh[t] = A.hi;
+            sAl[t] = A.lo;
+            sHh[t] = H.hi;
+            sHl[t] = H.lo;
+        }
+        __syncthreads();
+    }
+    DD s = t == 0 ? DD{0.0, 0.0} : DD{sHh[t - 1], sHl[t - 1]};  // s before the run (s_{-1} = 0)
+    for (long long k = a; k < e; ++k) {
+        cb[k] = ScanCarry{s.hi, s.lo};
+        const ScanTileMap q = mb[k];
+        s = dd_mul_add(TA, s, DD{q.Hhi, q.Hlo});
+    }
+}
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(SCAN_WARPS * 32)
+    scan_replay_kernel(const __grid_constant__ LevelC<T, NT> L, const T *f, T *u, long long n, int batch,
+                       long long tiles_per, const ScanCarry *carry, const int *active)
+{
+    constexpr int G = ScanTile<T, NT>::GROUPS;
+    constexpr int LOGW = 31 - __builtin_clz((unsigned)ScanTile<T, NT>::WARP_SLABS);
+    __shared__ double sh[SCAN_WARPS], sl[SCAN_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const ScanPowers P = scan_powers(DD{(double)L.calpha, L.calpha_lo}, LOGW);
+    // alpha^(lane+1): a lane's inclusive multiplier within its group
+    DD laneA_dd{1.0, 0.0};
 #pragma unroll
-        for (int j = 0; j < SCAN_GROUPS; ++j) {
-            // valid lanes' inclusive multiplier is alpha^(lane+1) in every group
-            const DD s_incl = dd_mul_add(laneA, sin, iH[j]);
-            DD s_prev{__shfl_up_sync(0xffffffffu, s_incl.hi, 1), __shfl_up_sync(0xffffffffu, s_incl.lo, 1)};
-            if (lane == 0) s_prev = sin;
+    for (int q = 0; q < 5; ++q)
+        if ((lane + 1) & (1 << q)) laneA_dd = dd_mul(laneA_dd, P.p[q]);
+    if (lane == 31) laneA_dd = P.p[5];
+    const double laneA = laneA_dd.hi;
+    const long long total = tiles_per * batch;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        const long long b = t / tiles_per, tile = t - b * tiles_per;
+        if (active && !active[b]) continue;
+        T g[G][NT];
+        double iH[G];
+        const long long s0 = tile * ScanTile<T, NT>::SLABS + warp * ScanTile<T, NT>::WARP_SLABS;
+        const DD WH = scan_warp<T, NT>(L, P, f + (size_t)b * n * NT, n, s0, lane, g, iH);
+        if (lane == 0) {
+            sh[warp] = WH.hi;
+            sl[warp] = WH.lo;
+        }
+        __syncthreads();
+        // this warp's incoming s: the tile's, then the preceding warps' maps
+        DD sin{carry[t].hi, carry[t].lo};
+        for (int w = 0; w < warp; ++w) sin = dd_mul_add(P.p[LOGW], sin, DD{sh[w], sl[w]});
+        __syncthreads();
+        T *ub = u + (size_t)b * n * NT;
+        double sg = __dadd_rn(sin.hi, sin.lo);  // the warp's incoming s, then each group's (local)
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const double s_incl = __fma_rn(laneA, sg, iH[j]);  // s after this lane's slab
+            double s_prev = __shfl_up_sync(0xffffffffu, s_incl, 1);
+            if (lane == 0) s_prev = sg;
             const long long k = s0 + 32LL * j + lane;
             if (k < n) {
                 T o[NT];
 #pragma unroll
-                for (int i = 0; i < NT; ++i)
-                    o[i] = (T)__fma_rn(s_prev.hi, (double)L.cw[i],
-                                       __fma_rn(s_prev.lo, (double)L.cw[i], (double)g[j][i]));
+                for (int i = 0; i < NT; ++i) o[i] = (T)__fma_rn(s_prev, (double)L.cw[i], (double)g[j][i]);
                 store_slab<T, NT>(ub + k * NT, o);
             }
-            sin = DD{__shfl_sync(0xffffffffu, s_incl.hi, 31), __shfl_sync(0xffffffffu, s_incl.lo, 31)};
+            sg = __shfl_sync(0xffffffffu, s_incl, 31);
         }
     }
 }

@@ -570,10 +570,15 @@ def run_gpu_arm(args, w):
     max_it = max(max(r) for r in iters)
     launches_per_step = 3 + info["kernels_per_cycle"] * max_it
 
-    # e2e: through the public API with HOST buffers (pinned): the C ABI's
-    # tmg_plan_solve_host copies F and the zero guess in and the solution out
+    # e2e: through the public API with HOST buffers (pinned): every step copies
+    # its batch in (H2D) and its solution out (D2H).  Headline: the streamed
+    # API (solve_batched_stream -> tmg_plan_solve_host_stream), which overlaps
+    # step k's solve with step k+1's copy-in and step k-1's copy-out; beside
+    # it the one-call-per-step form (tmg_plan_solve_host: the batch's copies
+    # overlap its own sub-batch solves only)
     F_host = F.cpu().pin_memory()
     U_host = torch.empty_like(F_host).pin_memory()
+    U_ring = [U_host] + [torch.empty_like(F_host).pin_memory() for _ in range(2)]
 
     def e2e_step():
         # zero initial guess (not copied), solution written into pinned U_host
@@ -591,14 +596,34 @@ def run_gpu_arm(args, w):
         dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = args.steps
-    dof_e2e = 0.0
+    dof_call = 0.0
     f0.record()
     for _ in range(e2e_steps):
         st = e2e_step()
-        dof_e2e += sum(n * nt * s.iterations for s in st)
+        dof_call += sum(n * nt * s.iterations for s in st)
     f1.record()
     torch.cuda.synchronize()
-    e2e_time = f0.elapsed_time(f1) * 1e-3
+    call_time = f0.elapsed_time(f1) * 1e-3
+    call_time, dof_call = tdist.reduce_time_and_work(call_time, dof_call, device="cuda")
+
+    # streamed: the K steps' batches through one call (warm-up stream first)
+    floors_k = [floors] * max(args.warmup, 1)
+    solver.solve_batched_stream(hier, [F_host] * len(floors_k), [U_ring[k % 3] for k in range(len(floors_k))],
+                                cfg, floors=floors_k)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    g0.record()
+    _, st_all = solver.solve_batched_stream(hier, [F_host] * e2e_steps,
+                                            [U_ring[k % 3] for k in range(e2e_steps)], cfg,
+                                            floors=[floors] * e2e_steps)
+    g1.record()
+    torch.cuda.synchronize()
+    e2e_wall = time.perf_counter() - w0
+    e2e_time = max(g0.elapsed_time(g1) * 1e-3, e2e_wall)
+    dof_e2e = float(sum(n * nt * s.iterations for st in st_all for s in st))
     e2e_time, dof_e2e = tdist.reduce_time_and_work(e2e_time, dof_e2e, device="cuda")
 
     # roofline of the dominant kernel, timed live on the plan's own launches:
@@ -656,9 +681,12 @@ def run_gpu_arm(args, w):
                          "coarse_pairs": l1},
             "e2e": {"value": dof_e2e / e2e_time, "unit": UNIT,
                     "h2d_bytes_per_step": B * n * nt * 8, "d2h_bytes_per_step": B * n * nt * 8,
-                    "steps": e2e_steps, "path": "DevicePlan.solve_host -> C ABI tmg_plan_solve_host with pinned "
-                    "host buffers: H2D f, solve (zero guess), D2H u; 16 pipelined sub-batches "
-                    "(copy-in / copy-out streams, three compute streams) overlap copies with solves"},
+                    "steps": e2e_steps, "path": "solve_batched_stream -> C ABI tmg_plan_solve_host_stream "
+                    "with pinned host buffers: every step copies its batch in (H2D f) and its solution out "
+                    "(D2H u); step k's solve overlaps step k+1's copy-in and step k-1's copy-out "
+                    "(copy-in, compute, copy-out streams; three full-batch plans in rotation)",
+                    "per_call": {"value": dof_call / call_time, "path": "one tmg_plan_solve_host call per step "
+                                 "(16 pipelined sub-batches within the step)"}},
             "gpu_launches": launches_per_step * args.steps,
             "parity": parity,
             "clocks": clk.summary(),

@@ -202,6 +202,18 @@ int tmg_plan_solve(tmg_plan *plan, const void *f, void *u, const double *floor_p
 int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, const void *u_init_host, void *u_host,
                         const double *floor_per_problem, double eps, int max_iters);
 
+/* A stream of n_batches independent batches through host buffers, each
+ * [batch][n_slabs][n_t] from the zero initial guess (the host-side call for
+ * a producer of many right-hand-side batches): pipelined ACROSS batches --
+ * batch k+1 is copied in and batch k-1 copied out while batch k is solved --
+ * so in steady state a batch costs max(solve, H2D, D2H).  floor_per_problem:
+ * [n_batches][batch]; results per batch: iterations[n_batches][batch],
+ * norms[n_batches][batch][max_iters + 1], converged[n_batches][batch] (any of
+ * the three may be NULL).  Blocks until every batch is done. */
+int tmg_plan_solve_host_stream(tmg_plan *plan, int n_batches, const void *const *f_hosts, void *const *u_hosts,
+                               const double *floor_per_problem, double eps, int max_iters, int32_t *iterations,
+                               double *norms, int32_t *converged);
+
 /* Results of the last tmg_plan_solve (host arrays):
  * iterations[batch], norms[batch * (max_iters + 1)] (first iterations[b]+1
  * valid per problem), converged[batch]. */

@@ -11,6 +11,7 @@ from .assembly import (ALPHA_MIN, BasisSpec, BlockLU, GlobalSystem, LocalOperato
 from .hierarchy import CycleConfig, Level, SolveStats, TimeHierarchy
 from .solver import (DevicePlan, block_jacobi_sweep, forward_solve, measure_convergence_factor,
                      measure_convergence_factors, random_initial_guess, solve, solve_batched,
+                     solve_batched_stream,
                      two_grid_cycle, v_cycle)
 from .rhs import rhs_moments_device, rhs_moments_samples, rhs_moments_sines
 

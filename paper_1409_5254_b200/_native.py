@@ -146,7 +146,8 @@ EXPORTS = ("tmg_last_error", "tmg_version", "tmg_device_check", "tmg_sweep", "tm
            "tmg_down", "tmg_up", "tmg_coarse_solve", "tmg_resid_norm", "tmg_resid_sqsum", "tmg_trace_enable", "tmg_trace_read", "tmg_plan_create",
            "tmg_plan_create_multi",
            "tmg_plan_destroy", "tmg_plan_cycles", "tmg_plan_solve", "tmg_plan_solve_host",
-           "tmg_plan_stats", "tmg_plan_info", "tmg_rhs_samples", "tmg_rhs_sines", "tmg_rhs_last_error")
+           "tmg_plan_stats", "tmg_plan_info", "tmg_rhs_samples", "tmg_rhs_sines", "tmg_rhs_last_error",
+           "tmg_plan_solve_host_stream")
 
 
 def load():
@@ -181,6 +182,8 @@ def load():
     L.tmg_plan_solve.argtypes = [vp, vp, vp, dp, ctypes.c_double, ci, vp]
     L.tmg_plan_solve_host.argtypes = [vp, vp, vp, vp, dp, ctypes.c_double, ci]
     L.tmg_plan_stats.argtypes = [vp, i32p, dp, i32p]
+    L.tmg_plan_solve_host_stream.argtypes = [vp, ci, ctypes.POINTER(vp), ctypes.POINTER(vp), dp,
+                                             ctypes.c_double, ci, i32p, dp, i32p]
     L.tmg_plan_info.argtypes = [vp, i32p, i32p, i32p]
     L.tmg_rhs_last_error.restype = ctypes.c_char_p
     L.tmg_rhs_samples.argtypes = [vp, vp, dp, dp, dp, ci, ci, vp, i64, i64, vp]

@@ -396,6 +396,8 @@ struct PlanBase {
                            int max_iters) = 0;
     virtual int stats(int32_t *it, double *norms, int32_t *conv) const = 0;
     virtual int info(int32_t *kpc, int32_t *sl, int32_t *tl) const = 0;
+    virtual int solve_host_stream(int nb, const void *const *f, void *const *u, const double *floor_, double eps,
+                                  int max_iters, int32_t *it, double *norms, int32_t *conv) = 0;
 };
 
 }  // namespace
@@ -490,6 +492,8 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         if (hp_st) cudaFreeHost(hp_st);
         if (hp_hist) cudaFreeHost(hp_hist);
         if (ev_done) cudaEventDestroy(ev_done);
+        if (ev_small_in) cudaEventDestroy(ev_small_in);
+        if (ev_solved) cudaEventDestroy(ev_solved);
     }
 
     size_t fixed_smem() const { return tail_fixed_smem<T, NT>(depth - tl); }
@@ -1122,10 +1126,50 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         else CK(cudaMemsetAsync(d_uh, 0, bytes, cin));
         CK(cudaEventRecord(ev_h2d, cin));
         CK(cudaStreamWaitEvent(cmp, ev_h2d, 0));
-        CKR(enqueue_solve(d_fh, d_uh, floor_, eps, max_iters, cmp));  // records ev_done on cmp
-        CK(cudaStreamWaitEvent(cout, ev_done, 0));
+        // the small floor/stat copies ride on the copy streams (see enqueue_solve);
+        // ev_done is recorded on cout after them
+        CKR(enqueue_solve(d_fh, d_uh, floor_, eps, max_iters, cmp, cin, cout));
         CK(cudaMemcpyAsync(u_out, d_uh, bytes, cudaMemcpyDeviceToHost, cout));
         CK(cudaEventRecord(ev_done, cout));  // collect() waits for the solution on the host
+        return 0;
+    }
+
+    // A stream of independent batches, each solved whole (the full-batch
+    // graph) from the zero guess, pipelined ACROSS batches: while batch k is
+    // solved, batch k+1 is copied in and batch k-1 copied out (copy-in,
+    // compute and copy-out streams; three full-batch plans in rotation, each
+    // with its own device buffers and graph), so the PCIe traffic hides under
+    // the solves and a batch costs max(solve, H2D, D2H) in steady state.
+    std::vector<std::unique_ptr<Plan>> ring;
+    int solve_host_stream(int nb, const void *const *f, void *const *u, const double *floor_, double eps,
+                          int max_iters, int32_t *it, double *norms, int32_t *conv) override
+    {
+        if (nb < 1) return fail(TMG_E_ARG, "need at least one batch");
+        if (ring.empty()) {
+            for (int k = 0; k < 3; ++k) {
+                auto p = std::make_unique<Plan>();
+                CKR(p->init(descs.data(), depth, B, o));
+                ring.push_back(std::move(p));
+            }
+        }
+        if (!cs_in) {
+            CK(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
+            for (int k = 0; k < 4; ++k) CK(cudaStreamCreateWithFlags(&cs_cmp[k], cudaStreamNonBlocking));
+        }
+        const int stride = max_iters + 1;
+        auto gather = [&](int k) -> int {
+            Plan &p = *ring[k % 3];
+            CKR(p.collect());
+            return p.stats(it ? it + (size_t)k * B : nullptr, norms ? norms + (size_t)k * B * stride : nullptr,
+                           conv ? conv + (size_t)k * B : nullptr);
+        };
+        for (int k = 0; k < nb; ++k) {
+            if (k >= 3) CKR(gather(k - 3));
+            CKR(ring[k % 3]->enqueue_host_async((const T *)f[k], nullptr, (T *)u[k], floor_ + (size_t)k * B, eps,
+                                                 max_iters, cs_in, cs_cmp[0], cs_out));
+        }
+        for (int k = std::max(0, nb - 3); k < nb; ++k) CKR(gather(k));
         return 0;
     }
 
@@ -1244,16 +1288,31 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     // enqueue a whole solve on stream s; the stopping state and the residual
     // histories land in pinned host buffers (collect() reads them)
-    int enqueue_solve(const void *f, void *u, const double *floor_, double eps, int max_iters, cudaStream_t s)
+    // s: the solve's kernels.  s_in / s_out (default s): the small copies of
+    // the stopping floors in and the statistics out -- a pipelined caller puts
+    // them on its copy streams, so the compute stream holds kernels only and a
+    // copy engine busy with another batch's bulk transfer never delays a solve
+    cudaEvent_t ev_small_in = nullptr, ev_solved = nullptr;
+    int enqueue_solve(const void *f, void *u, const double *floor_, double eps, int max_iters, cudaStream_t s,
+                      cudaStream_t s_in = nullptr, cudaStream_t s_out = nullptr)
     {
         if (max_iters < 1) return fail(TMG_E_ARG, "max_iters must be >= 1");
         CKR(ensure_hist(max_iters));
         if (ev_done) CK(cudaEventSynchronize(ev_done));  // the staging buffers are free again
+        if (!ev_small_in) {
+            CK(cudaEventCreateWithFlags(&ev_small_in, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_solved, cudaEventDisableTiming));
+        }
+        const cudaStream_t si = s_in ? s_in : s, so = s_out ? s_out : s;
         last_max_iters = max_iters;
         memcpy(hp_floor, floor_, sizeof(double) * B);
         for (long long b = 0; b < B; ++b) hp_init[b] = ProbState{0.0, 0, 1, max_iters, 0};
-        CK(cudaMemcpyAsync(d_floor, hp_floor, sizeof(double) * B, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(d_st, hp_init, sizeof(ProbState) * B, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_floor, hp_floor, sizeof(double) * B, cudaMemcpyHostToDevice, si));
+        CK(cudaMemcpyAsync(d_st, hp_init, sizeof(ProbState) * B, cudaMemcpyHostToDevice, si));
+        if (si != s) {
+            CK(cudaEventRecord(ev_small_in, si));
+            CK(cudaStreamWaitEvent(s, ev_small_in, 0));
+        }
         if (tl == 0) {
             TailArgs<T, NT> t = targ;
             t.f_in = (const T *)f;
@@ -1286,9 +1345,13 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
                 ++it;
             }
         }
-        CK(cudaMemcpyAsync(hp_st, d_st, sizeof(ProbState) * B, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(hp_hist, d_hist, sizeof(double) * hist_stride * B, cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(ev_done, s));
+        if (so != s) {
+            CK(cudaEventRecord(ev_solved, s));
+            CK(cudaStreamWaitEvent(so, ev_solved, 0));
+        }
+        CK(cudaMemcpyAsync(hp_st, d_st, sizeof(ProbState) * B, cudaMemcpyDeviceToHost, so));
+        CK(cudaMemcpyAsync(hp_hist, d_hist, sizeof(double) * hist_stride * B, cudaMemcpyDeviceToHost, so));
+        CK(cudaEventRecord(ev_done, so));
         return 0;
     }
 
@@ -1688,6 +1751,19 @@ int tmg_plan_solve_host(tmg_plan *plan, const void *f_host, const void *u_init_h
     if (!plan || !f_host || !u_host) return fail(TMG_E_ARG, "NULL argument");
     if (!(eps > 0.0 && eps < 1.0)) return fail(TMG_E_ARG, "eps must lie in (0, 1)");
     return plan->impl->solve_host(f_host, u_init_host, u_host, floor_per_problem, eps, max_iters);
+}
+
+int tmg_plan_solve_host_stream(tmg_plan *plan, int n_batches, const void *const *f_hosts, void *const *u_hosts,
+                               const double *floor_per_problem, double eps, int max_iters, int32_t *iterations,
+                               double *norms, int32_t *converged)
+{
+    if (!plan || !f_hosts || !u_hosts || !floor_per_problem) return fail(TMG_E_ARG, "NULL argument");
+    if (!(eps > 0.0 && eps < 1.0)) return fail(TMG_E_ARG, "eps must lie in (0, 1)");
+    if (max_iters < 1) return fail(TMG_E_ARG, "max_iters must be >= 1");
+    for (int k = 0; k < n_batches; ++k)
+        if (!f_hosts[k] || !u_hosts[k]) return fail(TMG_E_ARG, "batch %d: NULL host buffer", k);
+    return plan->impl->solve_host_stream(n_batches, f_hosts, u_hosts, floor_per_problem, eps, max_iters, iterations,
+                                         norms, converged);
 }
 
 int tmg_plan_stats(const tmg_plan *plan, int32_t *iterations, double *norms, int32_t *converged)

@@ -222,6 +222,24 @@ class DevicePlan:
             "tmg_plan_solve_host")
         return self._stats(max_iters)
 
+    def solve_host_stream(self, F_hosts, U_hosts, floors, eps: float, max_iters: int):
+        """Batches of host buffers (pinned for full PCIe speed) from the zero
+        guess, pipelined across batches (tmg_plan_solve_host_stream).
+        Returns per batch (iterations[B], norms[B, max_iters+1], converged[B])."""
+        nb = len(F_hosts)
+        fl = np.ascontiguousarray(np.broadcast_to(np.asarray(floors, dtype=np.float64), (nb, self.batch)))
+        fp = (ctypes.c_void_p * nb)(*[_host_ptr(x) for x in F_hosts])
+        up = (ctypes.c_void_p * nb)(*[_host_ptr(x) for x in U_hosts])
+        it = np.zeros((nb, self.batch), dtype=np.int32)
+        conv = np.zeros((nb, self.batch), dtype=np.int32)
+        norms = np.zeros((nb, self.batch, max_iters + 1))
+        nat.check(nat.load().tmg_plan_solve_host_stream(
+            self._h, nb, fp, up, fl.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(eps),
+            int(max_iters), it.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            conv.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), "tmg_plan_solve_host_stream")
+        return [(it[k], norms[k], conv[k]) for k in range(nb)]
+
     def _stats(self, max_iters):
         it = np.zeros(self.batch, dtype=np.int32)
         conv = np.zeros(self.batch, dtype=np.int32)
@@ -467,6 +485,40 @@ def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None, inp
     it, norms, conv = plan.solve(Fd, Ud, floors, config.eps, config.max_iters)
     elapsed = time.perf_counter() - t0
     return _out(Ud, was_t), _batched_stats(it, norms, conv, elapsed, config)
+
+
+def solve_batched_stream(hier, F_batches, U_outs=None, config: CycleConfig = None, floors=None):
+    """Many independent batches (host arrays (B, N, n_t), ideally pinned), each
+    solved from the zero guess exactly like ``solve_batched``, with the PCIe
+    copies of neighbouring batches overlapping each solve.  Returns
+    (U_outs, [[SolveStats] per batch])."""
+    config = config or CycleConfig()
+    depth = depth_of(hier, config)
+    if depth < 2:
+        raise ValueError("solve_batched_stream needs at least 2 levels")
+    N, nt = hier.finest.n_steps, hier.finest.ops.n_t
+    F_batches = list(F_batches)
+    if not F_batches:
+        raise ValueError("no batches")
+    B = int(F_batches[0].shape[0])
+    shape = (B, N, nt)
+    for F in F_batches:
+        if not _is_host(F) or tuple(F.shape) != shape:
+            raise ValueError(f"every batch must be a host array of shape {shape}")
+    Fh = [_host_array(F, copy=False) for F in F_batches]
+    if U_outs is None:
+        U_outs = [np.empty(shape) for _ in Fh]
+    elif len(U_outs) != len(Fh) or any(not _is_host(U) or tuple(U.shape) != shape for U in U_outs):
+        raise ValueError(f"U_outs must be {len(Fh)} host arrays of shape {shape}")
+    if floors is None:
+        floors = [[1e-12 * float(np.linalg.norm(np.asarray(F[b], dtype=np.float64))) for b in range(B)]
+                  for F in Fh]
+    _check_device()
+    plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, B)
+    t0 = time.perf_counter()
+    res = plan.solve_host_stream(Fh, U_outs, floors, config.eps, config.max_iters)
+    elapsed = time.perf_counter() - t0
+    return U_outs, [_batched_stats(it, norms, conv, elapsed / len(Fh), config) for it, norms, conv in res]
 
 
 def _batched_stats(it, norms, conv, elapsed, config):

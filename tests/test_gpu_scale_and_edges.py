@@ -339,3 +339,30 @@ def test_tail_cycle_sparse_forcing(oracle_mod, p_t, n):
         got = tmg.v_cycle(hier, u0, f, cfg)
         want = oracle_mod.cycle(hier, omegas(hier), u0, f, 1, 2)
         assert same_bits(got, want)
+
+
+def test_solve_batched_stream_matches_batched(oracle_mod):
+    """Batches through the cross-batch pipeline (tmg_plan_solve_host_stream)
+    equal separate solves: iterates, norms and counts."""
+    import torch
+    n, B, nb = 1 << 13, 4, 5
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(1), 1.0 / n, n, coarsest=2)
+    cfg = tmg.CycleConfig(nu1=1, nu2=1, eps=1e-8)
+    batches = [np.stack([problems.seeded_rhs(1, n, 1.0, 42, k * B + b)[0] for b in range(B)])
+               for k in range(nb)]
+    outs, stats = tmg.solve_batched_stream(hier, batches, None, cfg)
+    assert len(outs) == nb and len(stats) == nb
+    for k in range(nb):
+        Ud, st_d = tmg.solve_batched(hier, torch.from_numpy(batches[k]).cuda(), None, cfg)
+        assert same_bits(outs[k], Ud.cpu().numpy())
+        for b in range(B):
+            assert stats[k][b].iterations == st_d[b].iterations
+            assert stats[k][b].residual_norms == st_d[b].residual_norms
+    ur, norms, iters = oracle_mod.iterate(hier, omegas(hier), batches[3][1], np.zeros((n, 2)), 1, 1, 1e-8, 250)
+    assert same_bits(outs[3][1], ur) and stats[3][1].residual_norms == norms
+    # the same host output buffer reused across batches (written in stream order)
+    U = np.empty((B, n, 2))
+    outs2, _ = tmg.solve_batched_stream(hier, batches[:2], [U, U], cfg)
+    assert same_bits(outs2[1], outs[1])
+    with pytest.raises(ValueError):
+        tmg.solve_batched_stream(hier, [batches[0][:, :-1]], None, cfg)

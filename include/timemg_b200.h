@@ -159,7 +159,7 @@ typedef struct tmg_plan tmg_plan;
 typedef struct tmg_plan_opts {
     int32_t dtype;        /* TMG_F64 / TMG_F32 */
     int32_t nu1, nu2;     /* CycleConfig.nu1/nu2 */
-    int32_t gamma;        /* 1 = V-cycle (reference), 2 = W-cycle */
+    int32_t gamma;        /* cycle kind: 1 = V-cycle (reference), 2 = W-cycle, 3 = F-cycle */
     int32_t coarse;       /* 0 = serial (bitwise), 1 = scan, 2 = auto */
     int32_t dot_variant;  /* see tmg_coarse_solve */
     int32_t use_graph;    /* capture one cycle in a CUDA graph */

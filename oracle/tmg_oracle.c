@@ -297,17 +297,23 @@ typedef struct {
     int depth;                 /* levels used by the cycle */
     const tmo_level *lev;      /* [depth] */
     const int64_t *n;          /* slabs per level */
-    int nu1, nu2, gamma;       /* gamma = 1: V-cycle (reference); 2: W-cycle */
+    int nu1, nu2, gamma;       /* cycle kind: 1 V-cycle (reference); 2 W-cycle; 3 F-cycle */
     int dot_variant;
     double *u[TMO_MAXLEV][2];
     double *f[TMO_MAXLEV];
     double *r[TMO_MAXLEV];
 } tmo_ws;
 
-/* _cycle (multigrid.py:263-330), serial-slab form.  gamma = 2 repeats the
- * coarse-grid recursion (W-cycle; not in the reference, SPEC.md:430 -- this
- * composition of the reference's own steps is the documented oracle for it). */
-static int tmo_cycle_rec(tmo_ws *w, int lev, int cur)
+/* _cycle (multigrid.py:263-330), serial-slab form.  Kinds beyond the
+ * reference's V-cycle (not in the reference, SPEC.md:430 -- these
+ * compositions of the reference's own steps are the documented oracle for
+ * them): W (kind 2) visits the coarser level twice, both visits W-cycles; F
+ * (kind 3) visits it twice, an F-cycle and then a V-cycle.  The coarsest
+ * level is solved once per visit of its parent whatever the kind. */
+static int tmo_cycle_visits(int kind) { return kind == 1 ? 1 : 2; }
+static int tmo_cycle_child(int kind, int visit) { return (kind == 3 && visit > 0) ? 1 : kind; }
+
+static int tmo_cycle_rec(tmo_ws *w, int lev, int cur, int kind)
 {
     const tmo_level *L = &w->lev[lev];
     const int nt = L->nt;
@@ -325,8 +331,9 @@ static int tmo_cycle_rec(tmo_ws *w, int lev, int cur)
         ccur = 0;
     } else {
         memset(w->u[lev + 1][0], 0, sizeof(double) * (size_t)(w->n[lev + 1] * nt));
-        ccur = tmo_cycle_rec(w, lev + 1, 0);
-        for (int g = 1; g < w->gamma; ++g) ccur = tmo_cycle_rec(w, lev + 1, ccur);
+        ccur = 0;
+        for (int g = 0; g < tmo_cycle_visits(kind); ++g)
+            ccur = tmo_cycle_rec(w, lev + 1, ccur, tmo_cycle_child(kind, g));
     }
     tmo_prolong_add(L, w->u[lev + 1][ccur], w->u[lev][cur], 0, n / 2);
     for (int k = 0; k < w->nu2; ++k) {
@@ -364,7 +371,7 @@ static void ws_free(tmo_ws *w)
 int tmo_cycle(const tmo_level *lev, const int64_t *n, int depth, int nu1, int nu2, int gamma,
               int dot_variant, const double *u_in, const double *f, double *u_out)
 {
-    if (depth < 2 || depth > TMO_MAXLEV) return -1;
+    if (depth < 2 || depth > TMO_MAXLEV || gamma < 1 || gamma > 3) return -1;
     tmo_ws w;
     memset(&w, 0, sizeof w);
     w.depth = depth; w.lev = lev; w.n = n;
@@ -373,7 +380,7 @@ int tmo_cycle(const tmo_level *lev, const int64_t *n, int depth, int nu1, int nu
     size_t sz = sizeof(double) * (size_t)(n[0] * lev[0].nt);
     memcpy(w.u[0][0], u_in, sz);
     memcpy(w.f[0], f, sz);
-    int cur = tmo_cycle_rec(&w, 0, 0);
+    int cur = tmo_cycle_rec(&w, 0, 0, gamma);
     memcpy(u_out, w.u[0][cur], sz);
     ws_free(&w);
     return 0;
@@ -395,7 +402,7 @@ int tmo_iterate(const tmo_level *lev, const int64_t *n, int depth, int nu1, int 
                 int dot_variant, const double *f, const double *u_init, double eps, double floor_,
                 int max_iters, double *u_out, double *norms_out, int *n_norms)
 {
-    if (depth < 2 || depth > TMO_MAXLEV) return -1;
+    if (depth < 2 || depth > TMO_MAXLEV || gamma < 1 || gamma > 3) return -1;
     tmo_ws w;
     memset(&w, 0, sizeof w);
     w.depth = depth; w.lev = lev; w.n = n;
@@ -411,7 +418,7 @@ int tmo_iterate(const tmo_level *lev, const int64_t *n, int depth, int nu1, int 
     double tol = eps * r0 > floor_ ? eps * r0 : floor_;
     double rk = r0;
     while (rk > tol && iters < max_iters) {
-        cur = tmo_cycle_rec(&w, 0, cur);
+        cur = tmo_cycle_rec(&w, 0, cur, gamma);
         rk = norm_at(&w, sq, cur);
         iters += 1;
         norms_out[k++] = rk;

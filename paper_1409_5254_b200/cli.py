@@ -31,6 +31,8 @@ import time
 
 import numpy as np
 
+from .hierarchy import CYCLES
+
 EXIT_OK, EXIT_USAGE, EXIT_NOT_CONVERGED = 0, 2, 3
 
 
@@ -80,7 +82,7 @@ SOLVE_OPTS = (
     Opt("--seed", "seed", int, 42, "seed of the random initial guess"),
     Opt("--workers", "workers", int, 1, "accepted for compatibility (the GPU ignores it)"),
     Opt("--max-iters", "max_iters", int, 250, "cycle limit"),
-    Opt("--cycle", "cycle", str, "V", "cycle type (GPU addition)", ("V", "W")),
+    Opt("--cycle", "cycle", str, "V", "cycle type (GPU addition)", CYCLES),
 )
 
 BENCH_OPTS = (

@@ -506,7 +506,9 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         B = batch;
         o = opts;
         descs.assign(lv, lv + nl);
-        if (o.gamma < 1) o.gamma = 1;
+        if (o.gamma == 0) o.gamma = 1;
+        if (o.gamma < 1 || o.gamma > 3)
+            return fail(TMG_E_ARG, "gamma (cycle kind) must be 1 (V), 2 (W) or 3 (F), got %d", o.gamma);
         for (int l = 0; l < nl; ++l) {
             n.push_back(lv[l].n_slabs);
             L.push_back(make_level<T, NT>(lv[l]));
@@ -679,26 +681,36 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
 
     // coarse-grid correction of level l and its up pass (norm_up: the up pass
     // also produces the norm of its output -- used when the down pass cannot)
+    // ckind: this level's cycle (1 V, 2 W, 3 F; 0 = the plan's): a W visits
+    // level l+1 twice with W-cycles, an F with an F-cycle then a V-cycle (the
+    // oracle's tmo_cycle_rec); the coarsest level is solved once per visit
+    static int cycle_visits(int kind) { return kind == 1 ? 1 : 2; }
+    static int child_kind(int kind, int visit) { return (kind == 3 && visit > 0) ? 1 : kind; }
     int enqueue_rest(int l, const void *f0, void *u0, bool norm_up, cudaStream_t s, bool first_visit = true,
-                     bool fuse_next_down = false, bool skip_up = false, bool child_skip_down = false)
+                     bool fuse_next_down = false, bool skip_up = false, bool child_skip_down = false,
+                     int ckind = 0)
     {
+        if (ckind == 0) ckind = o.gamma;
         const T *fL = l == 0 ? (const T *)f0 : fl[l];
-        const bool pr = !skip_up && pair_up(l, first_visit);
+        const bool pr = !skip_up && pair_up(l, first_visit, ckind);
         if (l + 1 == tl) {
             TailArgs<T, NT> t = targ;
             t.f_in = fl[tl];
             t.u_in = nullptr;
             t.u_out = uA[tl];
             t.full = 0;
-            t.n_cycles = (tl == depth - 1) ? 1 : o.gamma;
+            t.n_cycles = (tl == depth - 1) ? 1 : cycle_visits(ckind);
+            t.gamma = ckind;
+            t.each_kind = 0;
             t.active = d_active;
             CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");
             trace_mark("tail_kernel", s);
             ++kernels_per_cycle;
         } else {
-            for (int g = 0; g < o.gamma; ++g)
-                CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s, pr, child_skip_down && g == 0));
+            for (int g = 0; g < cycle_visits(ckind); ++g)
+                CKR(enqueue_level(l + 1, f0, u0, g == 0, false, s, pr, child_skip_down && g == 0,
+                                  child_kind(ckind, g)));
         }
         if (skip_up) return 0;  // this level's up pass runs inside the next finer level's pass
         if (pr) {
@@ -774,12 +786,12 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
     }
 
     int enqueue_level(int l, const void *f0, void *u0, bool first_visit, bool norm, cudaStream_t s,
-                      bool skip_up = false, bool skip_down = false)
+                      bool skip_up = false, bool skip_down = false, int ckind = 0)
     {
         if (up2 && norm && !(l == 0 && norm_up2())) {
             // the up pass cannot produce the norm: take it in a separate pass
             CKR(enqueue_down(l, f0, u0, first_visit, false, s));
-            CKR(enqueue_rest(l, f0, u0, false, s, first_visit));
+            CKR(enqueue_rest(l, f0, u0, false, s, first_visit, false, false, false, ckind));
             return enqueue_norm_pass(f0, u0, s);
         }
         bool dp = false;
@@ -788,7 +800,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             if (dp) CKR(enqueue_down_pair(l, s, false));  // levels l and l+1
             else CKR(enqueue_down(l, f0, u0, first_visit, false, s));
         }
-        return enqueue_rest(l, f0, u0, norm, s, first_visit, false, skip_up, dp);
+        return enqueue_rest(l, f0, u0, norm, s, first_visit, false, skip_up, dp, ckind);
     }
 
     // standalone ||f - L u|| pass at the finest level (r0 / generic sizes)
@@ -827,20 +839,22 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
         return v == 1;
     }
     // coarse pairs (level l+1's up pass inside level l's, both from the zero
-    // guess; TMG_NO_VPAIR=1 disables)
-    bool pair_up(int l, bool first_visit) const
+    // guess; V-cycles only: measured on config 4 F/W with nu = 2 the pairs
+    // cost 10-20 % there; TMG_NO_VPAIR=1 disables)
+    bool pair_up(int l, bool first_visit, int ckind) const
     {
         static int v = -1;
         if (v < 0) {
             const char *e = getenv("TMG_NO_VPAIR");
             v = (e && *e && *e != '0') ? 0 : 1;
         }
-        return v == 1 && up2 && SP && o.gamma == 1 && o.nu1 <= 2 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
+        return v == 1 && up2 && SP && ckind == 1 && o.gamma == 1 && o.nu1 <= 2 && first_visit && l >= 1 && l + 1 < tl && pair_rows_ok() &&
                sizeof(T) == 8 && n[l] % (2 * ROWW) == 0 && pk[l] == pk[l + 1] && aligned16(fl[l]) &&
                aligned16(fl[l + 1]) && aligned16(uA[l]) && aligned16(uA[l + 2]);
     }
     // coarse down pairs (level l's down pass feeding level l+1's through shared
-    // memory, both from the zero guess; TMG_NO_DPAIR=1 disables)
+    // memory, both from the zero guess; V-cycles only, see pair_up;
+    // TMG_NO_DPAIR=1 disables)
     bool pair_down(int l, bool first_visit) const
     {
         static int v = -1;
@@ -1251,6 +1265,7 @@ template <typename T, int NT, bool SP> struct Plan : PlanBase {
             t.u_out = (T *)u;
             t.full = 0;
             t.n_cycles = nc;
+            t.each_kind = 1;
             t.active = nullptr;
             CK(((cudaError_t)tail_launch<T, NT>(t, SP, (unsigned)B, tail_smem_bytes, s)));
             CK_LAUNCH("tail_kernel");

@@ -542,25 +542,33 @@ template <typename T, int NT, bool SPARSE, bool SMEM> struct Engine {
         tick(3, l);
     }
 
-    // the rest of a gamma-cycle whose down pass at lstart is done
-    // (multigrid.py:263-330; gamma = 2: the W-cycle of the oracle's
-    // tmo_cycle_rec), iterative: cnt[l] = visits of level l+1 so far
-    __device__ void cycle_rest(int lstart, int last, int nu1, int nu2, int gamma, int variant)
+    // the rest of a cycle of the given kind (1 V, 2 W, 3 F) whose down pass
+    // at lstart is done (multigrid.py:263-330 for V; W and F as the oracle's
+    // tmo_cycle_rec: a W visits the coarser level twice with W-cycles, an F
+    // with an F-cycle and then a V-cycle), iterative: cnt[l] = visits of
+    // level l+1 so far, kd[l] = the kind of level l's current cycle
+    __device__ static int visits(int kind) { return kind == 1 ? 1 : 2; }
+    __device__ static int child_kind(int kind, int visit) { return (kind == 3 && visit > 0) ? 1 : kind; }
+    __device__ void cycle_rest(int lstart, int last, int nu1, int nu2, int kind, int variant)
     {
         int cnt[MAXLEV];
+        unsigned char kd[MAXLEV];
         int l = lstart;
         cnt[l] = 0;
+        kd[l] = (unsigned char)kind;
         while (true) {
             if (l + 1 == last) {
                 coarse_level(last, variant);
-                cnt[l] = gamma;
+                cnt[l] = visits(kd[l]);
             }
-            if (cnt[l] < gamma) {
+            if (cnt[l] < visits(kd[l])) {
                 const bool zg = cnt[l] == 0;  // first visit: zero initial guess (:311-312)
+                const int ck = child_kind(kd[l], cnt[l]);
                 cnt[l] += 1;
                 l += 1;
                 down(l, zg, nu1, false);
                 cnt[l] = 0;
+                kd[l] = (unsigned char)ck;
                 continue;
             }
             up(l, nu2);
@@ -628,12 +636,16 @@ __device__ void tail_body(const TailArgs<T, NT> &a)
     const int last = a.depth - 1;
 
     if (!a.full) {
+        // each_kind: n_cycles cycles of kind gamma; else gamma is the kind of
+        // the calling (streamed) level's cycle and its n_cycles visits of
+        // level l0 are cycles of the child kinds
         for (int c = 0; c < a.n_cycles; ++c) {
             if (a.l0 == last) {
                 E.coarse_level(last, a.dot_variant);
             } else {
                 E.down(a.l0, c == 0 && !a.u_in, a.nu1, false);
-                E.cycle_rest(a.l0, last, a.nu1, a.nu2, a.gamma, a.dot_variant);
+                const int kind = a.each_kind ? a.gamma : E.child_kind(a.gamma, c);
+                E.cycle_rest(a.l0, last, a.nu1, a.nu2, kind, a.dot_variant);
             }
         }
     } else {

@@ -52,7 +52,9 @@ template <typename T, int NT> struct TailArgs {
     T *u_out;                     // u at l0 after the work
     T *gstore;                    // global level store when not in shared memory
     int in_smem;
-    int nu1, nu2, gamma, dot_variant;
+    int nu1, nu2, dot_variant;
+    int gamma;                    // cycle kind (1 V, 2 W, 3 F): full mode, each_kind; else the caller's
+    int each_kind;                // cycle mode: 1 = every cycle is of kind gamma; 0 = the caller's visits
     int coarse_scan;              // coarsest solve by the CTA scan (not bitwise)
     int levels_stride;            // 0: one operator for the batch; else problem b's levels at b*stride
     unsigned long long *trace;    // optional: per-phase SM-cycle totals of problem 0 (diagnostics)

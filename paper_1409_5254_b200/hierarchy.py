@@ -5,7 +5,7 @@ unchanged (reference: pkg/src/timemg/multigrid.py):
   Level             multigrid.py:28-37
   TimeHierarchy     multigrid.py:40-80   (build: halve N, double tau while N
                                           is even and N/2 >= max(2, coarsest))
-  CycleConfig       multigrid.py:83-116  (+ ``cycle`` = "V" | "W", ``coarse``)
+  CycleConfig       multigrid.py:83-116  (+ ``cycle`` = "V" | "W" | "F", ``coarse``)
   SolveStats        multigrid.py:119-134
   _max_ratio        multigrid.py:418-424
 Nothing here touches the GPU.
@@ -69,7 +69,9 @@ class TimeHierarchy:
                 return cls(basis, out)
 
 
-CYCLES = ("V", "W")
+CYCLES = ("V", "W", "F")
+# cycle kind codes of the C ABI (TmgPlanOpts.gamma): V 1, W 2 (gamma = 2), F 3
+CYCLE_KIND = {"V": 1, "W": 2, "F": 3}
 COARSE_SOLVERS = ("auto", "serial", "scan")
 
 
@@ -77,8 +79,8 @@ COARSE_SOLVERS = ("auto", "serial", "scan")
 class CycleConfig:
     """Solver parameters; the reference fields keep their meaning and defaults.
 
-    Additions (not in the reference): ``cycle`` ("V", or "W" = gamma 2, see
-    DESIGN.md), ``coarse`` ("serial", the default: block forward substitution,
+    Additions (not in the reference): ``cycle`` ("V"; "W" = gamma 2; "F" = an
+    F-cycle then a V-cycle on the coarser level), ``coarse`` ("serial", the default: block forward substitution,
     bitwise with the reference; "scan": parallel affine scan, ~1e-15 relative,
     opt-in; "auto": serial unless the coarsest level has > 16384 slabs) and
     ``dot_variant`` (the host-BLAS summation tree the reference's coarse solve

@@ -8,8 +8,8 @@ Same names, arguments, defaults, return values and errors as the reference:
   measure_convergence_factor(hier, config=None)        multigrid.py:534-544
   random_initial_guess(hier, seed)                     multigrid.py:503-506
 plus ``solve_batched`` (B independent right-hand sides sharing one operator,
-each stopping at its own iteration count) and the W-cycle via
-``CycleConfig(cycle="W")``.
+each stopping at its own iteration count) and the W- and F-cycles via
+``CycleConfig(cycle="W" | "F")``.
 
 Arrays may be numpy (host; results come back as numpy) or torch CUDA tensors
 (device-resident; results stay on the device).  Every numeric step runs in the
@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _native as nat
 from . import blas_tree
-from .hierarchy import CycleConfig, SolveStats, depth_of, level_omegas, max_ratio
+from .hierarchy import CYCLE_KIND, CycleConfig, SolveStats, depth_of, level_omegas, max_ratio
 
 _COARSE = {"serial": 0, "scan": 1, "auto": 2}
 # levels with at most this many slabs per problem run in the single-CTA engine
@@ -183,7 +183,7 @@ class DevicePlan:
         self.n0 = flat[0].n_slabs
         self.n_t = flat[0].n_t
         self.dtype = dtype
-        opts = nat.PlanOpts(dtype, config.nu1, config.nu2, 2 if config.cycle == "W" else 1,
+        opts = nat.PlanOpts(dtype, config.nu1, config.nu2, CYCLE_KIND[config.cycle],
                             _COARSE[config.coarse], blas_tree.resolve(config.dot_variant), int(use_graph),
                             int(TAIL_MAX))
         self._h = ctypes.c_void_p()
@@ -328,7 +328,7 @@ def two_grid_cycle(hier, level: int, u, f, config: CycleConfig = None):
 
 
 def v_cycle(hier, u, f, config: CycleConfig = None):
-    """One V-cycle (or W-cycle with config.cycle == "W") from the finest level
+    """One V-cycle (or W-/F-cycle with config.cycle == "W"/"F") from the finest level
     (multigrid.py:366-375)."""
     config = config or CycleConfig()
     depth = depth_of(hier, config)

@@ -138,7 +138,7 @@ def main():
     for r in out["config2"]:
         print("config2", r, flush=True)
     if not args.quick:
-        # V down to 2 slabs (the reference setting); V and W over a 1024-slab
+        # V and F down to 2 slabs (the reference setting); V and W over a 1024-slab
         # coarsest level solved by the parallel scan (a deep W-cycle visits the
         # 2-slab level 2^19 times per cycle -- inherently sequential, see DESIGN)
         out["config4"] = []
@@ -148,6 +148,7 @@ def main():
                 out["config4"].append(solve_case(2, 1 << 20, T, nu, "V", coarsest=1024, coarse="scan"))
                 out["config4"].append(solve_case(2, 1 << 20, T, nu, "W", coarsest=1024, coarse="scan",
                                                  reps=3))
+                out["config4"].append(solve_case(2, 1 << 20, T, nu, "F"))
         out["config4_deepW"] = [solve_case(2, 1 << 14, 1.0, 1, "W", reps=2)]
         for r in out["config4"] + out["config4_deepW"]:
             print("config4", r, flush=True)

@@ -62,7 +62,7 @@ def test_hierarchy_nesting_and_caps():
 
 def test_config_validation():
     for bad in (dict(nu1=0, nu2=0), dict(eps=1.5), dict(workers=0), dict(max_iters=0),
-                dict(levels=0), dict(cycle="F"), dict(coarse="lu")):
+                dict(levels=0), dict(cycle="X"), dict(coarse="lu")):
         with pytest.raises(ValueError):
             CycleConfig(**bad)
     with pytest.raises(ValueError):

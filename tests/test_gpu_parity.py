@@ -267,17 +267,35 @@ def test_streaming_odd_sizes_vs_oracle(oracle_mod, p_t, n, rule, nu):
     assert same_bits(u, ur)
 
 
-@pytest.mark.parametrize("n,p_t", [(1024, 1), (1 << 17, 2)])
-def test_w_cycle_vs_oracle(oracle_mod, n, p_t):
+@pytest.mark.parametrize("cycle", ["W", "F"])
+@pytest.mark.parametrize("n,p_t,nu", [(1024, 1, 1), (1 << 17, 2, 1), (1 << 15, 1, 2), (1 << 16, 3, 1)])
+def test_w_f_cycle_vs_oracle(oracle_mod, n, p_t, nu, cycle):
+    """W- and F-cycle solves (whole problem in the tail, and streamed levels
+    above it) bitwise against the oracle's tmo_cycle_rec compositions"""
     rhs, tau, _ = problems.seeded_rhs(p_t, n, 1.0, 42)
     hier = tmg.TimeHierarchy.build(tmg.BasisSpec(p_t), tau, n, coarsest=2)
-    cfg = tmg.CycleConfig(nu1=1, nu2=1, eps=1e-8, cycle="W")
+    cfg = tmg.CycleConfig(nu1=nu, nu2=nu, eps=1e-8, cycle=cycle)
     u, st = tmg.solve(hier, rhs, np.zeros_like(rhs), cfg)
-    ur, norms, iters = oracle_mod.iterate(hier, omegas(hier), rhs, np.zeros_like(rhs), 1, 1,
-                                          1e-8, 250, gamma=2)
+    ur, norms, iters = oracle_mod.iterate(hier, omegas(hier), rhs, np.zeros_like(rhs), nu, nu,
+                                          1e-8, 250, gamma=tmg.hierarchy.CYCLE_KIND[cycle])
     assert st.iterations == iters
     assert st.residual_norms == norms
     assert same_bits(u, ur)
+
+
+@pytest.mark.parametrize("n,p_t", [(512, 1), (1 << 14, 2)])
+def test_f_cycle_single_cycles(oracle_mod, n, p_t):
+    """v_cycle(config.cycle="F") from a random iterate: one F-cycle, then a
+    second on its output, bitwise against the oracle's cycle"""
+    rhs, tau, _ = problems.seeded_rhs(p_t, n, 1.0, 42)
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(p_t), tau, n, coarsest=2)
+    cfg = tmg.CycleConfig(nu1=1, nu2=1, cycle="F")
+    u = tmg.random_initial_guess(hier, 5)
+    for _ in range(2):
+        out = tmg.v_cycle(hier, u, rhs, cfg)
+        ref = oracle_mod.cycle(hier, omegas(hier), u, rhs, 1, 1, gamma=3)
+        assert same_bits(out, ref)
+        u = out
 
 
 def test_batched_independent_stopping(oracle_mod):

@@ -160,3 +160,24 @@ def test_dgemv_tree_calibration(golden):
         for k in range(0, 512, 7):
             for i in range(nt):
                 assert trees[nt](c[i], x[k]) + 0.0 == y[k, i]
+
+
+def test_cycle_kinds_compose(oracle_mod):
+    """The W (gamma 2) and F (kind 3) cycles are compositions of the reference's
+    own steps: on two levels every kind is the two-grid cycle; on
+    three levels F == W (the coarser level's two visits are both two-grid
+    cycles); on four levels F differs from both (its second visit of level 1
+    is a V-cycle, the W's a W-cycle)."""
+    n, p_t = 256, 1
+    rhs, tau, _ = problems.seeded_rhs(p_t, n, 1.0, 42)
+    hier = TimeHierarchy.build(BasisSpec(p_t), tau, n, coarsest=2)
+    from paper_1409_5254_b200.hierarchy import CycleConfig, level_omegas
+    om = level_omegas(hier, CycleConfig(), len(hier.levels))
+    u0 = np.random.default_rng(1).standard_normal(rhs.shape)
+    cyc = lambda g, d: oracle_mod.cycle(hier, om, u0, rhs, 1, 1, depth=d, gamma=g)
+    assert same_bits(cyc(3, 2), cyc(1, 2)) and same_bits(cyc(2, 2), cyc(1, 2))
+    assert same_bits(cyc(3, 3), cyc(2, 3))
+    f4, w4, v4 = cyc(3, 4), cyc(2, 4), cyc(1, 4)
+    assert not same_bits(f4, w4) and not same_bits(f4, v4)
+    with pytest.raises(AssertionError):
+        oracle_mod.cycle(hier, om, u0, rhs, 1, 1, depth=4, gamma=4)

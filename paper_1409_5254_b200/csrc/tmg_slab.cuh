@@ -26,6 +26,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifdef TMG_NO_EXPECT
+#define TMG_UNLIKELY(x) (x)
+#else
+#define TMG_UNLIKELY(x) __builtin_expect(!!(x), 0)
+#endif
+
 namespace tmg {
 
 template <typename T> struct FP;
@@ -620,6 +626,28 @@ template <typename T, int NT> __device__ __forceinline__ void lu_apply_ieee(cons
     }
 }
 
+// the exact fallback out of line: J permuted right-hand sides by value
+template <typename T, int NT, int J> struct LuPack { T v[J][NT]; };
+template <typename T, int NT> struct LuConst { T lu[NT * NT]; T rinv[NT]; };
+template <typename T, int NT, int J>
+__device__ __noinline__ LuPack<T, NT, J> lu_fallback_cold(LuPack<T, NT, J> y, LuConst<T, NT> c)
+{
+#pragma unroll 1
+    for (int q = 0; q < J; ++q) {
+#pragma unroll
+        for (int i = 1; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < i; ++j) y.v[q][i] = FP<T>::sub(y.v[q][i], FP<T>::mul(c.lu[i * NT + j], y.v[q][j]));
+#pragma unroll
+        for (int i = NT - 1; i >= 0; --i) {
+#pragma unroll
+            for (int j = i + 1; j < NT; ++j) y.v[q][i] = FP<T>::sub(y.v[q][i], FP<T>::mul(c.lu[i * NT + j], y.v[q][j]));
+            y.v[q][i] = divq_exact(y.v[q][i], c.lu[i * NT + i], c.rinv[i]);
+        }
+    }
+    return y;
+}
+
 // LU solve + damped update for J slabs whose permuted residuals y are given
 template <typename T, int NT, int J>
 __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], T (&y)[J][NT])
@@ -644,13 +672,32 @@ __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], 
         for (int i = 0; i < NT; ++i) ys[q][i] = y[q][i];
 #pragma unroll
     for (int q = 0; q < J; ++q) lu_apply_nb<T, NT>(L, y[q], bad);
-    if (__any_sync(0xffffffffu, bad)) {
+    if (TMG_UNLIKELY(__any_sync(0xffffffffu, bad))) {
+#ifndef TMG_INLINE_FALLBACK
+        // out of line (the hot loop's code stays dense); operands by value
+        LuPack<T, NT, J> in;
+        LuConst<T, NT> lc;
+#pragma unroll
+        for (int i = 0; i < NT * NT; ++i) lc.lu[i] = L.lu[i];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) lc.rinv[i] = L.rinv[i];
+#pragma unroll
+        for (int q = 0; q < J; ++q)
+#pragma unroll
+            for (int i = 0; i < NT; ++i) in.v[q][i] = ys[q][i];
+        LuPack<T, NT, J> out = lu_fallback_cold<T, NT, J>(in, lc);
+#pragma unroll
+        for (int q = 0; q < J; ++q)
+#pragma unroll
+            for (int i = 0; i < NT; ++i) y[q][i] = out.v[q][i];
+#else
 #pragma unroll
         for (int q = 0; q < J; ++q) {
 #pragma unroll
             for (int i = 0; i < NT; ++i) y[q][i] = ys[q][i];
             lu_apply_fallback<T, NT>(L, y[q]);
         }
+#endif
     }
 #pragma unroll
     for (int q = 0; q < J; ++q)

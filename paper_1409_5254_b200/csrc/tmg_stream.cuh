@@ -305,7 +305,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     T *leafbuf;              // per-warp numpy leaf buffer (SF_NORM_LEAF)
     int leaf_q;              // rows buffered in leafbuf
     int lb = LB;             // leaves per flush (the buffer's capacity)
-    long long leaf0;         // index of the first buffered leaf
+    long long leaf0;         // leaf_out index of the first buffered leaf (leaf_begin)
     long long nc;
     bool write_u;            // the pass stores u (u_out given)
     bool vec_out;            // u_out rows are 16-byte aligned (vector stores)
@@ -328,7 +328,8 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     __device__ __forceinline__ void leaf_flush(int b)
     {
         __syncwarp();
-        const int nl = leaf_q / a.leaf_rows;
+        // (no integer divisions on the full-buffer path: they are subroutine calls)
+        const int nl = leaf_q == lb * a.leaf_rows ? lb : leaf_q / a.leaf_rows;
         const int m = a.leaf_rows * W;
         const int l = lane >> 3, j = lane & 7;
         T acc = T(0);
@@ -340,14 +341,20 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         T t1 = FP<T>::add(acc, __shfl_down_sync(0xffffffffu, acc, 1));
         T t2 = FP<T>::add(t1, __shfl_down_sync(0xffffffffu, t1, 2));
         T t3 = FP<T>::add(t2, __shfl_down_sync(0xffffffffu, t2, 4));
-        const long long nleaves = a.n / ((long long)W * a.leaf_rows);
-        if (j == 0 && l < nl) a.leaf_out[(size_t)b * nleaves + leaf0 + l] = (double)t3;
+        if (j == 0 && l < nl) a.leaf_out[leaf0 + l] = (double)t3;
         __syncwarp();
         leaf_q = 0;
+        leaf0 += nl;
+    }
+    // leaf cursor of a warp whose first row is row0 (a multiple of leaf_rows):
+    // index into leaf_out of the next leaf to flush, advanced by every flush
+    __device__ __forceinline__ void leaf_begin(long long row0, int b)
+    {
+        leaf_q = 0;
+        leaf0 = (long long)b * (a.n / ((long long)W * a.leaf_rows)) + row0 / a.leaf_rows;
     }
     __device__ __forceinline__ void leaf_row(const T (&r)[P][NT], long long row, int b)
     {
-        if (leaf_q == 0) leaf0 = row / a.leaf_rows;
         T sq[P];
 #pragma unroll
         for (int q = 0; q < P; ++q) sq[q] = sqnorm<T, NT>(r[q]);
@@ -409,7 +416,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
             for (int q = 0; q < P; ++q) nz |= neg_zero_rows<T, NT>(f[q]);
             // (inlined: an out-of-line exact path would take the row arrays
             // by reference and force them into local memory -- 3x slower)
-            if (__any_sync(0xffffffffu, nz)) {
+            if (TMG_UNLIKELY(__any_sync(0xffffffffu, nz))) {
                 row_impl<INTERIOR, true>(u, f, uc, slab0, row_idx, warm, b, uo, fco, zg);
                 return;
             }
@@ -640,6 +647,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     }
     st.leaf_q = 0;
     st.leaf0 = 0;
+    if (KindLeaf<KIND>::value && st.has(SF_NORM_LEAF)) st.leaf_begin(row0, b);
 
     // groups [0, g_full) consist of G whole rows (and go through the ring when
     // TMA is on); groups [g_int0, g_full) are interior (no slab 0, all valid)
@@ -861,6 +869,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     for (int k = 0; k <= S1::NPRE + NU; ++k) cpl_zero(s1.carry[k]);
     st.leaf_q = 0;
     st.leaf0 = 0;
+    if constexpr (FINEST) st.leaf_begin(row0, b);
     st.halo_w = nullptr;
     st.write_u = true;
     st.vec_out = true;

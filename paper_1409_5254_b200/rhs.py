@@ -79,7 +79,7 @@ def rhs_moments_samples(fvals, basis, tau: float, u0=0.0):
     c, w, start = quadrature(basis, tau)
     if s != len(c):
         raise ValueError(f"fvals has {s} samples per step, the rule has {len(c)} nodes")
-    u0s = np.broadcast_to(np.asarray(u0, dtype=np.float64), (B,))
+    u0s = np.array(np.broadcast_to(np.asarray(u0, dtype=np.float64), (B,)))  # writable copy for torch
     u0d = torch.from_numpy(np.ascontiguousarray(u0s)).cuda() if np.any(u0s != 0.0) else None
     out = torch.empty((B, n, basis.n_t), dtype=torch.float64, device="cuda")
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -110,7 +110,7 @@ def rhs_moments_sines(basis, tau: float, n_steps: int, amp, phase, T: float = 1.
     B, K = amp2.shape
     c, w, start = quadrature(basis, tau)
     freq = sine_frequencies(K)
-    u0s = np.broadcast_to(np.asarray(u0, dtype=np.float64), (B,))
+    u0s = np.array(np.broadcast_to(np.asarray(u0, dtype=np.float64), (B,)))  # writable copy for torch
     ad = torch.from_numpy(np.ascontiguousarray(amp2)).cuda()
     pd = torch.from_numpy(np.ascontiguousarray(ph2)).cuda()
     u0d = torch.from_numpy(np.ascontiguousarray(u0s)).cuda() if np.any(u0s != 0.0) else None

@@ -7,9 +7,9 @@ OUT=$1; shift
 for rep in 1 2; do
   for v in "$@"; do
     if [ "$v" = default ]; then LIB=""; else LIB="TMG_LIB=$PWD/build/$v/libtimemg_b200.so"; fi
-    echo "[$v] config3 $(env $LIB timeout 300 python scripts/trace_solve.py 64 22 1 2>&1 | head -1)" >> $OUT
+    echo "[$v] config3 $(env $LIB timeout 300 python scripts/trace_solve.py 64 22 1 2>&1 | grep "graph solve")" >> $OUT
     for pt in 1 3; do
-      echo "[$v] config2 p_t=$pt $(env $LIB timeout 120 python scripts/trace_solve.py 1 20 $pt 2>&1 | head -1)" >> $OUT
+      echo "[$v] config2 p_t=$pt $(env $LIB timeout 120 python scripts/trace_solve.py 1 20 $pt 2>&1 | grep "graph solve")" >> $OUT
     done
   done
 done

@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 #include <numeric>
@@ -31,6 +33,43 @@
 #include "tmg_stream.cuh"  // StreamArgs / flags / kinds (kernels are instantiated in tmg_inst.cu)
 
 using namespace tmg;
+
+namespace tmg {
+
+void *scan_workspace(size_t bytes, cudaStream_t s, bool *owned)
+{
+    *owned = false;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+        *owned = true;
+        return p;
+    }
+    struct Ws {
+        void *p = nullptr;
+        size_t bytes = 0;
+    };
+    static std::mutex mu;
+    static std::unordered_map<unsigned long long, Ws> per_stream;   // (device, stream)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    Ws &w = per_stream[((unsigned long long)(uintptr_t)s << 8) ^ (unsigned long long)dev];
+    if (w.bytes < bytes) {
+        if (w.p) cudaFree(w.p);   // synchronises: no kernel still reads the old buffer
+        const size_t want = std::max<size_t>(bytes, 1 << 16);
+        if (cudaMalloc(&w.p, want) != cudaSuccess) {
+            w.p = nullptr;
+            w.bytes = 0;
+            return nullptr;
+        }
+        w.bytes = want;
+    }
+    return w.p;
+}
+
+}  // namespace tmg
 
 namespace {
 

@@ -3,6 +3,7 @@
 //   -DTMG_T=double|float -DTMG_NT=1..4
 // A translation unit of its own: edits of the tail rebuild nothing else.
 #define TMG_INST_UNIT 1
+#include <cstdlib>
 #include "tmg_launch.cuh"
 #include "tmg_tail.cuh"
 #include "tmg_scan.cuh"
@@ -41,31 +42,80 @@ int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, 
     return (int)cudaGetLastError();
 }
 
-// exact solve by the grid-wide three-pass scan (tmg_scan.cuh): tile maps and
-// carries in a stream-ordered allocation
+// exact solve by the grid-wide three-pass scan (tmg_scan.cuh): the runs' maps /
+// carries (one array, converted in place) in a stream-ordered allocation
 template <typename T, int NT>
 int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, int batch, const int *active,
                        cudaStream_t s)
 {
     if (n <= 0 || batch <= 0) return 0;
-    const long long tiles_per = (n + ScanTile<T, NT>::SLABS - 1) / ScanTile<T, NT>::SLABS;
-    const size_t maps_bytes = sizeof(ScanTileMap) * (size_t)tiles_per * batch;
-    const size_t carry_bytes = sizeof(ScanCarry) * (size_t)tiles_per * batch;
-    void *ws = nullptr;
-    cudaError_t e = cudaMallocAsync(&ws, maps_bytes + carry_bytes, s);
-    if (e != cudaSuccess) return (int)e;
-    auto *maps = reinterpret_cast<ScanTileMap *>(ws);
-    auto *carry = reinterpret_cast<ScanCarry *>(static_cast<char *>(ws) + maps_bytes);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned ctas = (unsigned)std::min<long long>(tiles_per * batch, (long long)sms * 4);
-    scan_agg_kernel<T, NT><<<ctas, SCAN_WARPS * 32, 0, s>>>(L, f, n, batch, tiles_per, maps, active);
-    scan_carry_kernel<T, NT><<<(unsigned)batch, SCAN_CARRY_THREADS, 0, s>>>(L, tiles_per, maps, carry, active);
-    scan_replay_kernel<T, NT><<<ctas, SCAN_WARPS * 32, 0, s>>>(L, f, u, n, batch, tiles_per, carry, active);
-    e = cudaGetLastError();
-    cudaError_t e2 = cudaFreeAsync(ws, s);
-    return (int)(e != cudaSuccess ? e : e2);
+    const long long tiles_per = (n + ScanTile<T, NT>::SLABS - 1) / ScanTile<T, NT>::SLABS;
+    // tiles per run: at most SCAN_MAX_RUNS runs per problem and at most 32
+    // tiles per run; among those the value that leaves the resident warps
+    // (2 CTAs per SM, static grid-stride) the least uneven share, ties to
+    // the longer run (fewer maps)
+    const long long warps = (long long)sms * 2 * SCAN_WARPS;
+    const long long cap = (tiles_per + SCAN_MAX_RUNS - 1) / SCAN_MAX_RUNS;
+    int run = (int)cap;
+    long long best = -1;
+    for (long long c = cap; c <= std::max<long long>(cap, 32); ++c) {
+        const long long runs = ((tiles_per + c - 1) / c) * batch;
+        const long long worst = ((runs + warps - 1) / warps) * c;   // tiles of the busiest warp
+        if (best < 0 || worst <= best) {
+            best = worst;
+            run = (int)c;
+        }
+    }
+    if (const char *ev = getenv("TMG_SCAN_RUN")) {   // experiments
+        const int v = atoi(ev);
+        if (v >= cap && v <= 64) run = v;
+    }
+    const long long runs_per = (tiles_per + run - 1) / run;
+    // workspace: the runs' maps, converted to carries in place
+    bool ws_owned = false;
+    void *ws = scan_workspace(sizeof(double) * (size_t)runs_per * batch, s, &ws_owned);
+    if (!ws) return (int)cudaErrorMemoryAllocation;
+    cudaError_t e = cudaSuccess;
+    auto *maps = reinterpret_cast<double *>(ws);
+    const int cth = scan_carry_threads(runs_per);
+    const int lgS = scan_carry_logm4((int)runs_per, cth) + 2;
+    const size_t stage_bytes = sizeof(double) * (size_t)(runs_per + (runs_per >> lgS) + 1);
+    // two transpose buffers per warp; padded so that at most two CTAs share an
+    // SM whatever n_t: with room to spare, the NEXT kernel's CTAs (programmatic
+    // dependent launch) become resident early and shrink the L1 under the
+    // running pass (p_t = 0: 532 us instead of 331 us at 4 x 2^24)
+    const size_t tile_bytes = std::max<size_t>(sizeof(T) * 2 * SCAN_WARPS * ScanTile<T, NT>::WARP_ELEMS, 80 * 1024);
+    static bool attr_done = false;
+    if (!attr_done) {
+        e = cudaFuncSetAttribute(scan_agg_kernel<T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_bytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(scan_replay_kernel<T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tile_bytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(scan_carry_kernel<T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * (SCAN_MAX_RUNS + SCAN_MAX_RUNS / 4 + 2)));
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    const unsigned ctas = (unsigned)std::min<long long>((runs_per * batch + SCAN_WARPS - 1) / SCAN_WARPS,
+                                                       (long long)sms * 2);
+    e = launch_pdl(scan_agg_kernel<T, NT>, dim3(ctas), dim3(SCAN_WARPS * 32), tile_bytes, s, L, f, n, batch, runs_per,
+                   run, maps, active);
+    if (e == cudaSuccess)
+        e = launch_pdl(scan_carry_kernel<T, NT>, dim3((unsigned)batch), dim3(cth), stage_bytes, s, L, (int)runs_per,
+                       run, (const double *)maps, maps, active);
+    if (e == cudaSuccess)
+        e = launch_pdl(scan_replay_kernel<T, NT>, dim3(ctas), dim3(SCAN_WARPS * 32), tile_bytes, s, L, f, u, n, batch,
+                       runs_per, run, (const double *)maps, active);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (ws_owned) {
+        cudaError_t e2 = cudaFreeAsync(ws, s);
+        if (e == cudaSuccess) e = e2;
+    }
+    return (int)e;
 }
 
 template int coarse_scan_launch<TMG_T, TMG_NT>(const LevelC<TMG_T, TMG_NT> &, const TMG_T *, TMG_T *, long long,

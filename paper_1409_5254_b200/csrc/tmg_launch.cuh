@@ -64,6 +64,13 @@ int coarse_serial_launch(const LevelC<T, NT> &L, bool sparse, const T *f, T *u, 
 template <typename T, int NT>
 int coarse_scan_launch(const LevelC<T, NT> &L, const T *f, T *u, long long n, int batch, const int *active,
                        cudaStream_t s);
+// Workspace of the scan solve on stream s (defined in tmg_api.cu): one
+// grow-only device buffer per stream, reused by every call on that stream
+// (work on one stream is ordered).  A stream-ordered allocation per call
+// (cudaMallocAsync / cudaFreeAsync) cost 50-250 us and made the timings
+// erratic; it remains the path under stream capture, where *owned is set
+// and the caller frees with cudaFreeAsync.  nullptr on failure.
+void *scan_workspace(size_t bytes, cudaStream_t s, bool *owned);
 
 #define TMG_DECLARE(T, NT)                                                                              \
     extern template int stream_launch<T, NT>(const LevelC<T, NT> &, const StreamArgs<T> &, int, int, int, \

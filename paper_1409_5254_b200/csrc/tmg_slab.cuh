@@ -626,11 +626,11 @@ template <typename T, int NT> __device__ __forceinline__ void lu_apply_ieee(cons
     }
 }
 
-// the exact fallback out of line: J permuted right-hand sides by value
+// the exact fallback out of line: J permuted right-hand sides and the LU constants by value
 template <typename T, int NT, int J> struct LuPack { T v[J][NT]; };
 template <typename T, int NT> struct LuConst { T lu[NT * NT]; T rinv[NT]; };
 template <typename T, int NT, int J>
-__device__ __noinline__ LuPack<T, NT, J> lu_fallback_cold(LuPack<T, NT, J> y, LuConst<T, NT> c)
+__device__ __noinline__ LuPack<T, NT, J> lu_fallback_byvalue(LuPack<T, NT, J> y, LuConst<T, NT> c)
 {
 #pragma unroll 1
     for (int q = 0; q < J; ++q) {
@@ -674,7 +674,12 @@ __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], 
     for (int q = 0; q < J; ++q) lu_apply_nb<T, NT>(L, y[q], bad);
     if (TMG_UNLIKELY(__any_sync(0xffffffffu, bad))) {
 #ifndef TMG_INLINE_FALLBACK
-        // out of line (the hot loop's code stays dense); operands by value
+      if constexpr (NT <= 2) {
+        // out of line, so the hot loop's code stays dense (-3 % on the headline;
+        // n_t >= 3 would pass 20+ doubles and measured 5 % slower: inline there).
+        // Operands by value in registers: passing them through a local-memory
+        // block instead measured 4 % SLOWER (ptxas then reloads the level
+        // constants with LDC in the hot path).
         LuPack<T, NT, J> in;
         LuConst<T, NT> lc;
 #pragma unroll
@@ -685,19 +690,21 @@ __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], 
         for (int q = 0; q < J; ++q)
 #pragma unroll
             for (int i = 0; i < NT; ++i) in.v[q][i] = ys[q][i];
-        LuPack<T, NT, J> out = lu_fallback_cold<T, NT, J>(in, lc);
+        LuPack<T, NT, J> out = lu_fallback_byvalue<T, NT, J>(in, lc);
 #pragma unroll
         for (int q = 0; q < J; ++q)
 #pragma unroll
             for (int i = 0; i < NT; ++i) y[q][i] = out.v[q][i];
-#else
+      } else
+#endif
+      {
 #pragma unroll
         for (int q = 0; q < J; ++q) {
 #pragma unroll
             for (int i = 0; i < NT; ++i) y[q][i] = ys[q][i];
             lu_apply_fallback<T, NT>(L, y[q]);
         }
-#endif
+      }
     }
 #pragma unroll
     for (int q = 0; q < J; ++q)

@@ -391,11 +391,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
         carry[k] = x;
         if constexpr (TRACK) {
             if (lane == 31) {
-                if constexpr (NT == 2) {
-                    *reinterpret_cast<uint2 *>(rec + k * NT) =
-                        make_uint2((unsigned)__double2hiint((double)u[P - 1][0]),
-                                   (unsigned)__double2hiint((double)u[P - 1][1]));
-                } else {
+                {
 #pragma unroll
                     for (int j = 0; j < NT; ++j) rec[k * NT + j] = (unsigned)__double2hiint((double)u[P - 1][j]);
                 }
@@ -938,6 +934,10 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         __syncwarp();
     }
 
+    // loop invariants of the per-row bookkeeping as 32-bit row numbers
+    const int halo_rr = (FINEST && chunk + 1 < a.chunks) ? rows - 1 : -1;   // row whose result is the chunk's halo
+    T *halo_slot = FINEST ? halo_next + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT : nullptr;
+    const int first_rr = row0 == 0 ? 0 : -1;                               // the problem's first row (general path)
     for (int g = 0; g < ngroups; ++g) {
         const T *stg = ring + (size_t)(g % Lay::ST) * Lay::STAGE;
         mbar_wait(&bars[g % Lay::ST], (uint32_t)((g / Lay::ST) & 1));
@@ -965,11 +965,8 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
                 __syncwarp();
                 if (lane == 0 && g + Lay::ST < ngroups) issue(g + Lay::ST);
             }
-            if constexpr (FINEST)
-                st.halo_w = (rr == rows - 1 && chunk + 1 < a.chunks)
-                                ? halo_next + ((size_t)b * a.chunks + chunk) * Lay::ROW + lofs * NT
-                                : nullptr;
-            if (ridx > 0) st.template row<true>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, !FINEST);
+            if constexpr (FINEST) st.halo_w = rr == halo_rr ? halo_slot : nullptr;
+            if (rr != first_rr) st.template row<true>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, !FINEST);
             else st.template row<false>(u, f, uc, ridx * W + lofs, ridx, false, b, uo, fco, !FINEST);
             uo += Lay::ROW;
             if constexpr (FINEST) fco += Lay::HALF;

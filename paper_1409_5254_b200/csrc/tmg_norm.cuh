@@ -25,23 +25,62 @@ __global__ void __launch_bounds__(1024)
     long long per = m > T ? m / T : 1;
     int used = (int)(m > T ? T : m);
     if (t < used) {
-        // bottom-up perfect tree over [t*per, (t+1)*per)
-        double stack[40];
-        for (long long i = 0; i < per; ++i) {
-            double x = lv[t * per + i];
-            int l = 0;
-            while ((i >> l) & 1) { x = __dadd_rn(stack[l], x); ++l; }
-            stack[l] = x;
+        if (per <= 32) {
+            // the thread's perfect subtree in registers, 16 leaves at a time:
+            // all loads first (no dependent load chain), then log2 rounds of
+            // left + right; per = 32 is two such halves
+            const int p = (int)(per < 16 ? per : 16);
+            double half[2] = {0.0, 0.0};
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (hh * 16 < per) {
+                    double x[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) x[i] = i < p ? lv[(long long)t * per + hh * 16 + i] : 0.0;
+#pragma unroll
+                    for (int w = 1; w < 16; w <<= 1) {
+                        if (w < p) {
+#pragma unroll
+                            for (int i = 0; i < 16; i += 2 * w) x[i] = __dadd_rn(x[i], x[i + w]);
+                        }
+                    }
+                    half[hh] = x[0];
+                }
+            }
+            v = per > 16 ? __dadd_rn(half[0], half[1]) : half[0];
+        } else {
+            // bottom-up perfect tree over [t*per, (t+1)*per)
+            double stack[40];
+            for (long long i = 0; i < per; ++i) {
+                double x = lv[t * per + i];
+                int l = 0;
+                while ((i >> l) & 1) { x = __dadd_rn(stack[l], x); ++l; }
+                stack[l] = x;
+            }
+            int top = 0;
+            while ((1LL << top) < per) ++top;
+            v = stack[top];
         }
-        int top = 0;
-        while ((1LL << top) < per) ++top;
-        v = stack[top];
     }
-    part[t] = v;
+    // the threads' values: the same left + right tree, five levels per warp by
+    // shuffles (lane l holds node l of the level when l % (2 s) == 0), then
+    // the warps' sums by warp 0  (used is a power of two, as m and T are)
+#pragma unroll
+    for (int s2 = 1; s2 < 32; s2 <<= 1) {
+        const double o = __shfl_down_sync(0xffffffffu, v, s2);
+        if (s2 < used) v = __dadd_rn(v, o);
+    }
+    if ((t & 31) == 0) part[t >> 5] = v;
     __syncthreads();
-    for (int s = 1; s < used; s <<= 1) {
-        if ((t % (2 * s)) == 0 && t + s < used) part[t] = __dadd_rn(part[t], part[t + s]);
-        __syncthreads();
+    if (t < 32) {
+        const int nw = (used + 31) >> 5;
+        double w = t < nw ? part[t] : 0.0;
+#pragma unroll
+        for (int s2 = 1; s2 < 32; s2 <<= 1) {
+            const double o = __shfl_down_sync(0xffffffffu, w, s2);
+            if (s2 < nw) w = __dadd_rn(w, o);
+        }
+        if (t == 0) part[0] = w;
     }
     if (t == 0) {
         double nrm = __dsqrt_rn(part[0]);

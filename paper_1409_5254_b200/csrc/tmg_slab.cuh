@@ -71,13 +71,19 @@ template <typename T> __host__ __device__ constexpr bool fast_fp() { return size
 // the correctly rounded quotient; the remainders are exact fma results).
 // Outside a safe exponent window (zeros, subnormals, huge values) it defers to
 // the IEEE division, so the result always equals FP<T>::div(a, d) bit for bit.
+// the IEEE divisions of the rare paths, out of line: inline they are ~40
+// instructions each, and the single-CTA engine alone had 387 copies (640 KB of
+// code around a hot path of a few hundred instructions per level pass)
+static __device__ __noinline__ double ddiv_cold(double a, double d) { return __ddiv_rn(a, d); }
+static __device__ __noinline__ float fdiv_cold(float a, float d) { return __fdiv_rn(a, d); }
+
 __device__ __forceinline__ double divq(double a, double d, double rinv)
 {
     double q0 = __dmul_rn(a, rinv);
     double q1 = __fma_rn(__fma_rn(-q0, d, a), rinv, q0);
     double q2 = __fma_rn(__fma_rn(-q1, d, a), rinv, q1);
     const unsigned e = (unsigned)(__double2hiint(a) >> 20) & 0x7ffu;
-    if (__builtin_expect(e - 123u >= 1800u, 0)) q2 = __ddiv_rn(a, d);  // |a| outside [2^-900, 2^900)
+    if (__builtin_expect(e - 123u >= 1800u, 0)) q2 = ddiv_cold(a, d);  // |a| outside [2^-900, 2^900)
     return q2;
 }
 __device__ __forceinline__ float divq(float a, float d, float rinv)
@@ -86,7 +92,7 @@ __device__ __forceinline__ float divq(float a, float d, float rinv)
     float q1 = __fmaf_rn(__fmaf_rn(-q0, d, a), rinv, q0);
     float q2 = __fmaf_rn(__fmaf_rn(-q1, d, a), rinv, q1);
     const unsigned e = (__float_as_uint(a) >> 23) & 0xffu;
-    if (__builtin_expect(e - 28u >= 200u, 0)) q2 = __fdiv_rn(a, d);  // |a| outside [2^-99, 2^101)
+    if (__builtin_expect(e - 28u >= 200u, 0)) q2 = fdiv_cold(a, d);  // |a| outside [2^-99, 2^101)
     return q2;
 }
 
@@ -648,6 +654,25 @@ __device__ __noinline__ LuPack<T, NT, J> lu_fallback_byvalue(LuPack<T, NT, J> y,
     return y;
 }
 
+// the same for one slab with the level constants behind a pointer (the
+// single-CTA engine keeps them in shared memory): one pointer and n_t doubles
+// per call site instead of n_t^2 + 2 n_t doubles
+template <typename T, int NT>
+__device__ __noinline__ LuPack<T, NT, 1> lu_fallback_ptr(const LevelC<T, NT> *L, LuPack<T, NT, 1> y)
+{
+#pragma unroll
+    for (int i = 1; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j) y.v[0][i] = FP<T>::sub(y.v[0][i], FP<T>::mul(L->lu[i * NT + j], y.v[0][j]));
+#pragma unroll
+    for (int i = NT - 1; i >= 0; --i) {
+#pragma unroll
+        for (int j = i + 1; j < NT; ++j) y.v[0][i] = FP<T>::sub(y.v[0][i], FP<T>::mul(L->lu[i * NT + j], y.v[0][j]));
+        y.v[0][i] = divq_exact(y.v[0][i], L->lu[i * NT + i], L->rinv[i]);
+    }
+    return y;
+}
+
 // LU solve + damped update for J slabs whose permuted residuals y are given
 template <typename T, int NT, int J>
 __device__ __forceinline__ void finish_j(const LevelC<T, NT> &L, T (&u)[J][NT], T (&y)[J][NT])
@@ -891,9 +916,13 @@ __device__ __forceinline__ void sweep(const LevelC<T, NT> &L, T (&u)[NT], const 
     unsigned bad = 0;
     lu_apply_nb<T, NT>(L, y, bad);
     if (__builtin_expect(bad != 0, 0)) {
+        // per thread (no warp vote: the single-CTA engine's chunks differ), out of line
+        LuPack<T, NT, 1> in;
 #pragma unroll
-        for (int i = 0; i < NT; ++i) y[i] = ys[i];
-        lu_apply_fallback<T, NT>(L, y);
+        for (int i = 0; i < NT; ++i) in.v[0][i] = ys[i];
+        const LuPack<T, NT, 1> out = lu_fallback_ptr<T, NT>(&L, in);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) y[i] = out.v[0][i];
     }
 #pragma unroll
     for (int i = 0; i < NT; ++i) u[i] = FP<T>::add(FP<T>::mul(y[i], L.omega), u[i]);

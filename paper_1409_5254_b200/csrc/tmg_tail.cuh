@@ -270,9 +270,12 @@ template <typename T, int NT, bool SPARSE, bool SMEM> struct Engine {
             unsigned bad = 0;
             lu_apply_nb<T, NT>(L, y, bad);
             if (__builtin_expect(bad != 0, 0)) {
+                LuPack<T, NT, 1> in;
 #pragma unroll
-                for (int i = 0; i < NT; ++i) y[i] = ys[i];
-                lu_apply_fallback<T, NT>(L, y);
+                for (int i = 0; i < NT; ++i) in.v[0][i] = ys[i];
+                const LuPack<T, NT, 1> out = lu_fallback_ptr<T, NT>(&L, in);
+#pragma unroll
+                for (int i = 0; i < NT; ++i) y[i] = out.v[0][i];
             }
 #pragma unroll
             for (int i = 0; i < NT; ++i) u[0][i] = FP<T>::add(FP<T>::mul(y[i], L.omega), T(0));

@@ -21,6 +21,7 @@ with ``n_steps``, ``tau``, ``ops``, ``r1``, ``r2``; ``basis``).
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 
 import numpy as np
@@ -375,10 +376,50 @@ def _floor_of(f) -> float:
     return 1e-12 * float(np.linalg.norm(f))
 
 
+# SolveStats.times (multigrid.py:227-241 splits smoothing / transfer / coarse /
+# residual).  The fused kernels run several of the reference's phases in one
+# launch, so by default the device solve's wall time is reported under
+# "smoothing".  With PHASE_TIMES (or TMG_PHASE_TIMES=1) the solve runs under
+# the library's kernel trace (every kernel launched separately and timed with
+# CUDA events: slower than the graph-launched solve) and the kernel times are
+# split as
+#   "smoothing": the streaming level passes (sweeps fused with the residual,
+#                restriction and prolongation of the same pass: "transfer" is
+#                part of them and stays 0),
+#   "coarse":    the single-CTA engine (every level <= 1024 slabs and the
+#                coarsest-level solve),
+#   "residual":  norm finalisation, stopping test and its host round trip.
+PHASE_TIMES = os.environ.get("TMG_PHASE_TIMES", "") not in ("", "0")
+
+
 def _times(total: float) -> dict:
-    # the fused kernels do not separate the phases; the wall time of the
-    # device solve is reported under "smoothing"
     return {"smoothing": total, "transfer": 0.0, "coarse": 0.0, "residual": 0.0}
+
+
+def _phase_bucket(kernel_name: str) -> str:
+    if "tail" in kernel_name or "coarse" in kernel_name:
+        return "coarse"
+    if kernel_name.startswith("stream_kernel"):
+        return "smoothing"
+    return "residual"
+
+
+def _traced(call):
+    """Run call() under the kernel trace; returns (result, times dict)."""
+    L = nat.load()
+    L.tmg_trace_enable(1)
+    try:
+        out = call()
+        buf = ctypes.create_string_buffer(1 << 20)
+        L.tmg_trace_read(buf, len(buf))
+    finally:
+        L.tmg_trace_enable(0)
+    times = _times(0.0)
+    for line in buf.value.decode().splitlines():
+        name, _, ms = line.split("\t")
+        if name != "start":
+            times[_phase_bucket(name)] += 1e-3 * float(ms)
+    return out, times
 
 
 def solve(hier, f, u_init=None, config: CycleConfig = None):
@@ -399,12 +440,16 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
         floor = 1e-12 * float(np.linalg.norm(_to_numpy(f).astype(np.float64, copy=False)))
         plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, 1)
         t0 = time.perf_counter()
-        it, norms, conv = plan.solve_host(fh, uh, uh, [floor], config.eps, config.max_iters)
-        elapsed = time.perf_counter() - t0
+        if PHASE_TIMES:
+            (it, norms, conv), times = _traced(
+                lambda: plan.solve_host(fh, uh, uh, [floor], config.eps, config.max_iters))
+        else:
+            it, norms, conv = plan.solve_host(fh, uh, uh, [floor], config.eps, config.max_iters)
+            times = _times(time.perf_counter() - t0)
         k = int(it[0])
         hist = [float(v) for v in norms[0, :k + 1]]
         return uh, SolveStats(iterations=k, residual_norms=hist, factor=max_ratio(hist),
-                              times=_times(elapsed), converged=bool(conv[0]), seed=config.seed,
+                              times=times, converged=bool(conv[0]), seed=config.seed,
                               workers=config.workers)
     torch = _torch()
     fd, was_t = _dev_block(f, shape, "f")
@@ -422,12 +467,15 @@ def solve(hier, f, u_init=None, config: CycleConfig = None):
     plan = get_plan(hier, 0, depth, omegas, config, 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    it, norms, conv = plan.solve(fd, ud, [floor], config.eps, config.max_iters)
-    elapsed = time.perf_counter() - t0
+    if PHASE_TIMES:
+        (it, norms, conv), times = _traced(lambda: plan.solve(fd, ud, [floor], config.eps, config.max_iters))
+    else:
+        it, norms, conv = plan.solve(fd, ud, [floor], config.eps, config.max_iters)
+        times = _times(time.perf_counter() - t0)
     k = int(it[0])
     hist = [float(v) for v in norms[0, :k + 1]]
     stats = SolveStats(iterations=k, residual_norms=hist, factor=max_ratio(hist),
-                       times=_times(elapsed), converged=bool(conv[0]), seed=config.seed,
+                       times=times, converged=bool(conv[0]), seed=config.seed,
                        workers=config.workers)
     return _out(ud, was_t), stats
 

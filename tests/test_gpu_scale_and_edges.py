@@ -366,3 +366,25 @@ def test_solve_batched_stream_matches_batched(oracle_mod):
     assert same_bits(outs2[1], outs[1])
     with pytest.raises(ValueError):
         tmg.solve_batched_stream(hier, [batches[0][:, :-1]], None, cfg)
+
+
+def test_phase_times_split(oracle_mod):
+    """SolveStats.times with PHASE_TIMES: the traced solve (kernels launched
+    one by one) gives the same bits as the graph-launched one and splits the
+    device time over the reference's phase keys (multigrid.py:227-241)."""
+    from paper_1409_5254_b200 import solver
+    n = 1 << 15
+    rhs, tau, _ = problems.seeded_rhs(1, n, 1.0, 42)
+    hier = tmg.TimeHierarchy.build(tmg.BasisSpec(1), tau, n, coarsest=2)
+    cfg = tmg.CycleConfig(nu1=1, nu2=1, eps=1e-8)
+    u0, st0 = tmg.solve(hier, rhs, np.zeros_like(rhs), cfg)
+    assert set(st0.times) == {"smoothing", "transfer", "coarse", "residual"}
+    solver.PHASE_TIMES = True
+    try:
+        u1, st1 = tmg.solve(hier, rhs, np.zeros_like(rhs), cfg)
+    finally:
+        solver.PHASE_TIMES = False
+    assert u1.tobytes() == u0.tobytes() and st1.residual_norms == st0.residual_norms
+    assert set(st1.times) == {"smoothing", "transfer", "coarse", "residual"}
+    assert st1.times["smoothing"] > 0 and st1.times["coarse"] > 0 and st1.times["residual"] > 0
+    assert st1.times["transfer"] == 0.0

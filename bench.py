@@ -477,6 +477,62 @@ def run_config5(args, w):
         dist.destroy_process_group()
 
 
+def config5_side_line(rank, steps=10, warmup=3):
+    """BASELINE config 5 (the north-star gate: one fused pass of nu1 = 2 sweeps
+    + residual + restriction over N = 2^26 slabs, p_t = 3) measured beside the
+    headline, so that the default run carries it: fp64 GB/s against the HBM
+    peak with the reference's golden prefix hashes, fp32 beside it.  Its own
+    full line (e2e, CPU baseline): --workload config5."""
+    import torch
+    from paper_1409_5254_b200 import _native as nat, problems
+    w = WORKLOADS["config5"]
+    L = nat.load()
+    n, nt, nu = w["n"], w["p_t"] + 1, w["nu"]
+    ops, r1, r2, om = c5_level(w)
+    d = nat.level_desc(ops, n, om, r1, r2)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5000 + rank)
+    u = torch.randn((n, nt), generator=gen, device="cuda", dtype=torch.float64)
+    f = torch.randn((n, nt), generator=gen, device="cuda", dtype=torch.float64)
+    npre = 1 << 16
+    up, fp = problems.kernel_inputs(npre, nt, 0)
+    u[:npre].copy_(torch.from_numpy(up))
+    f[:npre].copy_(torch.from_numpy(fp))
+    uo = torch.empty_like(u)
+    fc = torch.empty((n // 2, nt), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def timed(dt, uu, ff, o, c):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for k in range(warmup + steps):
+            if k == warmup:
+                e0.record(stream)
+            nat.check(L.tmg_down(dt, ctypes.byref(d), P(ff), P(uu), P(o), P(c), 1, nu, None, sp), "tmg_down")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / steps
+
+    t64 = timed(0, u, f, uo, fc)
+    peak, _ = peak_hbm()
+    nbytes = C5_BYTES * nt * 8 * n
+    out = {"workload": "config5: tmg_down (nu1=2 sweeps + residual + restriction), N=2^26, p_t=3, inputs > L2",
+           "steps": steps, "warmup": warmup, "dtype": "f64", "launch_s": t64, "bytes_per_launch": nbytes,
+           "achieved": nbytes / t64 / 1e9, "peak": peak, "unit": "GB/s", "frac": nbytes / t64 / 1e9 / peak,
+           "parity": {"prefix_sha_u": _sha(uo[:npre].cpu().numpy()) == golden_c5()["sha_u"],
+                      "prefix_sha_fc": _sha(fc[:npre // 2].cpu().numpy()) == golden_c5()["sha_fc"]}}
+    u32, f32 = u.float(), f.float()
+    uo32, fc32 = torch.empty_like(u32), torch.empty_like(fc, dtype=torch.float32)
+    t32 = timed(1, u32, f32, uo32, fc32)
+    out["fp32"] = {"launch_s": t32, "achieved": nbytes / 2 / t32 / 1e9, "frac": nbytes / 2 / t32 / 1e9 / peak,
+                   "normwise_u": float(torch.linalg.norm(uo32.double() - uo) / torch.linalg.norm(uo)),
+                   "normwise_fc": float(torch.linalg.norm(fc32.double() - fc) / torch.linalg.norm(fc))}
+    out["parity"]["all"] = bool(out["parity"]["prefix_sha_u"] and out["parity"]["prefix_sha_fc"]
+                                and max(out["fp32"]["normwise_u"], out["fp32"]["normwise_fc"]) <= 1e-5)
+    return out
+
+
 def golden_c5():
     with open(GOLDEN) as fh:
         return json.load(fh)["config5"]
@@ -659,6 +715,15 @@ def run_gpu_arm(args, w):
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                "seconds": secs}
 
+    c5 = None
+    if rank == 0 and args.workload == "config3" and not args.no_config5:
+        del F, U
+        torch.cuda.empty_cache()
+        try:
+            c5 = config5_side_line(rank)
+        except Exception as exc:  # the headline line must still print
+            c5 = {"error": repr(exc)}
+
     if rank == 0:
         ms = 1e3 * elapsed / args.steps
         line = {
@@ -691,6 +756,7 @@ def run_gpu_arm(args, w):
             "parity": parity,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "config5": c5,
         }
         # whole-cycle HBM fraction over every problem-cycle of the run: this
         # design moves 7 n_t 8 B per finest slab per V-cycle (vertically fused
@@ -713,6 +779,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 side measurement")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     w = WORKLOADS[args.workload]

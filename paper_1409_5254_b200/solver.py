@@ -535,10 +535,24 @@ def solve_batched(hier, F, U0=None, config: CycleConfig = None, floors=None, inp
     return _out(Ud, was_t), _batched_stats(it, norms, conv, elapsed, config)
 
 
+def _stream_split(B: int) -> int:
+    """Sub-batches per batch in solve_batched_stream: the pipeline's fill (first
+    copy-in) and drain (last copy-out) are one sub-batch long, so finer is
+    better until the per-solve latency of the small levels shows.  B = 64 x 2^22,
+    time-DoF/s at 5 / 10 batches per call: split 1: 6.6e10 / 7.4e10, 2: 7.4e10 /
+    7.8e10, 4: 7.6e10 / 7.6e10, 8: 7.2e10 / 7.4e10 -- halves are the default
+    (TMG_STREAM_SPLIT overrides)."""
+    env = os.environ.get("TMG_STREAM_SPLIT", "")
+    if env:
+        s = max(1, int(env))
+        return s if B % s == 0 else 1
+    return 2 if B % 2 == 0 and B // 2 >= 16 else 1
+
+
 def solve_batched_stream(hier, F_batches, U_outs=None, config: CycleConfig = None, floors=None):
     """Many independent batches (host arrays (B, N, n_t), ideally pinned), each
     solved from the zero guess exactly like ``solve_batched``, with the PCIe
-    copies of neighbouring batches overlapping each solve.  Returns
+    copies of neighbouring (sub-)batches overlapping each solve.  Returns
     (U_outs, [[SolveStats] per batch])."""
     config = config or CycleConfig()
     depth = depth_of(hier, config)
@@ -562,10 +576,23 @@ def solve_batched_stream(hier, F_batches, U_outs=None, config: CycleConfig = Non
         floors = [[1e-12 * float(np.linalg.norm(np.asarray(F[b], dtype=np.float64))) for b in range(B)]
                   for F in Fh]
     _check_device()
-    plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, B)
+    split = _stream_split(B)
+    Bs = B // split
+    if split > 1:
+        # problems are independent: a batch is `split` consecutive sub-batches
+        # (contiguous views of the same host arrays) in the same pipeline
+        Fs = [F[i * Bs:(i + 1) * Bs] for F in Fh for i in range(split)]
+        Us = [U[i * Bs:(i + 1) * Bs] for U in U_outs for i in range(split)]
+        fl = [list(fb[i * Bs:(i + 1) * Bs]) for fb in floors for i in range(split)]
+    else:
+        Fs, Us, fl = Fh, U_outs, floors
+    plan = get_plan(hier, 0, depth, omegas_for(hier, config, depth), config, Bs)
     t0 = time.perf_counter()
-    res = plan.solve_host_stream(Fh, U_outs, floors, config.eps, config.max_iters)
+    res = plan.solve_host_stream(Fs, Us, fl, config.eps, config.max_iters)
     elapsed = time.perf_counter() - t0
+    if split > 1:
+        res = [tuple(np.concatenate([res[k * split + i][j] for i in range(split)]) for j in range(3))
+               for k in range(len(Fh))]
     return U_outs, [_batched_stats(it, norms, conv, elapsed / len(Fh), config) for it, norms, conv in res]
 
 

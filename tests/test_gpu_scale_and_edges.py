@@ -388,3 +388,43 @@ def test_phase_times_split(oracle_mod):
     assert set(st1.times) == {"smoothing", "transfer", "coarse", "residual"}
     assert st1.times["smoothing"] > 0 and st1.times["coarse"] > 0 and st1.times["residual"] > 0
     assert st1.times["transfer"] == 0.0
+
+
+@pytest.mark.parametrize("p_t", [0, 1, 2, 3])
+def test_scan_edges_guards_and_alignment(oracle_mod, p_t):
+    """grid-wide scan solve through the C ABI at sizes around the tile and run
+    boundaries (a tile is 256 slabs for n_t <= 2, 128 above), batched with
+    ragged ends, with the output inside guard regions (nothing outside u is
+    written) and with a right-hand side that is NOT 16-byte aligned (the
+    synchronous fetch path instead of cp.async)."""
+    import torch
+    nt = p_t + 1
+    L = nat.load()
+    ops = tmg.assemble_local(tmg.BasisSpec(p_t), 1e-3)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    guard = 64
+    for n, B in [(1, 1), (2, 3), (127, 2), (128, 1), (129, 2), (255, 1), (256, 2), (257, 3), (2047, 1),
+                 (2049, 2), (256 * 7 + 1, 2), (128 * 33 - 1, 3), (40000, 2)]:
+        rng = np.random.default_rng(1000 * p_t + n)
+        rhs = rng.standard_normal((B, n, nt))
+        d = nat.level_desc(ops, n)
+        for shift in (0, 1):   # shift = 1: f starts 8 bytes into its buffer
+            fbuf = torch.zeros(B * n * nt + 2, dtype=torch.float64, device="cuda")
+            fv = fbuf[shift:shift + B * n * nt]
+            fv.copy_(torch.from_numpy(rhs.reshape(-1)))
+            ubuf = torch.full((B * n * nt + 2 * guard,), float("nan"), dtype=torch.float64, device="cuda")
+            uv = ubuf[guard:guard + B * n * nt]
+            nat.check(L.tmg_coarse_solve(nat.F64, ctypes.byref(d), ctypes.c_void_p(fv.data_ptr()),
+                                         ctypes.c_void_p(uv.data_ptr()), B, 1, blas_tree.resolve(None), st),
+                      "tmg_coarse_solve")
+            torch.cuda.synchronize()
+            host = ubuf.cpu().numpy()
+            assert np.all(np.isnan(host[:guard])) and np.all(np.isnan(host[-guard:])), (n, B, shift)
+            got = host[guard:-guard].reshape(B, n, nt)
+            assert np.all(np.isfinite(got)), (n, B, shift)
+            for b in range(B):
+                exact = oracle_mod.forward_solve_extended(ops, rhs[b])
+                want = oracle_mod.forward_substitute(ops, rhs[b])
+                nrm = max(np.linalg.norm(exact), 1e-300)
+                assert np.linalg.norm(got[b] - exact) <= 1e-12 * nrm, (n, B, b, shift)
+                assert np.linalg.norm(got[b] - want) <= np.linalg.norm(want - exact) + 1e-12 * nrm

@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <string>
 
+#include <algorithm>
 #include "timemg_b200.h"
 
 namespace {
@@ -79,27 +80,52 @@ __device__ __forceinline__ void fold_u0(const RhsConst &c, double u0, double (&m
     }
 }
 
+// S consecutive samples of one slab (16-byte loads when the slab's samples
+// are a multiple of 16 bytes and the array is 16-byte aligned)
+template <int S> __device__ __forceinline__ void load_samples(const double *p, bool vec, double (&fv)[S])
+{
+    if constexpr (S % 2 == 0) {
+        if (vec) {
+#pragma unroll
+            for (int k = 0; k < S; k += 2) {
+                const double2 v = *reinterpret_cast<const double2 *>(p + k);
+                fv[k] = v.x;
+                fv[k + 1] = v.y;
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < S; ++k) fv[k] = p[k];
+}
+
+// grid: x over the slabs of a problem (grid-stride), y over the problems
+// (grid-stride) -- no integer division per element; one slab per thread and
+// step, loads and stores of a warp contiguous
 template <int NT, int S>
 __global__ void __launch_bounds__(256) rhs_samples_kernel(const __grid_constant__ RhsConst c, const double *fvals,
                                                           const double *u0, double *rhs, long long n,
-                                                          long long total)
+                                                          long long batch)
 {
-    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-         g += (long long)gridDim.x * blockDim.x) {
-        const long long slab = g % n;
-        double fv[S];
+    const bool vec = (reinterpret_cast<uintptr_t>(fvals) & 15) == 0 && ((n * S) % 2 == 0 || batch == 1);
+    for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
+        const double *fb = fvals + b * n * S;
+        double *rb = rhs + b * n * NT;
+        for (long long slab = (long long)blockIdx.x * blockDim.x + threadIdx.x; slab < n;
+             slab += (long long)gridDim.x * blockDim.x) {
+            double fv[S];
+            load_samples<S>(fb + slab * S, vec, fv);
+            double m[NT];
 #pragma unroll
-        for (int k = 0; k < S; ++k) fv[k] = fvals[g * S + k];
-        double m[NT];
+            for (int j = 0; j < NT; ++j) {
+                double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < S; ++k) acc = __fma_rn(fv[k], c.w[j * S + k], acc);
-            m[j] = acc;
+                for (int k = 0; k < S; ++k) acc = __fma_rn(fv[k], c.w[j * S + k], acc);
+                m[j] = acc;
+            }
+            if (slab == 0 && u0) fold_u0<NT>(c, u0[b], m);
+            store_moments<NT>(rb + slab * NT, m);
         }
-        if (slab == 0 && u0) fold_u0<NT>(c, u0[g / n], m);
-        store_moments<NT>(rhs + g * NT, m);
     }
 }
 
@@ -156,8 +182,16 @@ int launch(const RhsConst &c, const double *fvals, const double *amp, const doub
 {
     if (total == 0) return 0;
     const unsigned grid = grid_for(total);
-    if constexpr (SINES) rhs_sines_kernel<NT, S><<<grid, 256, 0, s>>>(c, amp, phase, u0, rhs, n, total);
-    else rhs_samples_kernel<NT, S><<<grid, 256, 0, s>>>(c, fvals, u0, rhs, n, total);
+    if constexpr (SINES) {
+        rhs_sines_kernel<NT, S><<<grid, 256, 0, s>>>(c, amp, phase, u0, rhs, n, total);
+    } else {
+        // x: the slabs of one problem, y: problems; together about the same
+        // number of CTAs as the flat grid
+        const long long batch = total / n;
+        const unsigned gx = (unsigned)std::min<long long>((n + 255) / 256, grid);
+        const unsigned gy = (unsigned)std::min<long long>(batch, std::max<long long>(1, grid / gx));
+        rhs_samples_kernel<NT, S><<<dim3(gx, std::min(gy, 65535u)), 256, 0, s>>>(c, fvals, u0, rhs, n, batch);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return rfail((int)e, cudaGetErrorString(e));
     return 0;

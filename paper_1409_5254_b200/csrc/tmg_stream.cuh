@@ -266,7 +266,9 @@ template <typename T, int NT, bool WITH_C, bool LEAF> struct RowLayout {
     static constexpr size_t SMEM_BYTES = BAR_BYTES + BYTES_PER_WARP * WARPS;
 };
 
-template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct Streamer {
+// RTREG: the restriction blocks (R1, R2) of a two-slab lane held in ordinary
+// registers, opaque to the compiler (see transfer_regs)
+template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM, bool RTREG = false> struct Streamer {
     using C = Cpl<T, NT, SPARSE>;
     static constexpr int CF = KIND == K_DOWN ? (SF_RESTRICT | SF_WRITE_U)
                               : KIND == K_UP ? (SF_PROLONG | SF_WRITE_U)
@@ -299,6 +301,7 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     static constexpr bool TRACK = SPARSE && !fast_fp<T>();
     static constexpr int NX = NPRE + NU + NPOST + 1;  // exchanges per row
     T Rm[RREG ? NT * NT : 1];
+    T Rr1[RTREG ? NT * NT : 1], Rr2[RTREG ? NT * NT : 1];
     const T *Rs;
     unsigned *rec;           // [NX][NT] (TRACK)
     C carry[NPRE + NU + NPOST + 1];  // lane 0: predecessor data of the next row, per sweep
@@ -311,6 +314,26 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
     bool vec_out;            // u_out rows are 16-byte aligned (vector stores)
     T *halo_w;               // K_UP2DOWN: this lane's slot of the chunk's halo row (last row only)
 
+    // ptxas treats kernel-parameter constants as uniform values: in the coarse
+    // down pairs it parks (R1, R2) in ordinary registers outside the row loop
+    // and then, every row, spills four uniform registers and moves the twelve
+    // halves back into uniform registers (R2UR) just to use each once as a
+    // uniform operand -- 20 of the pass's 284 instructions per row.  Values
+    // that came out of a shuffle are not "uniform" any more and are used
+    // straight from their registers.
+    __device__ __forceinline__ void transfer_regs()
+    {
+        if constexpr (RTREG) {
+#pragma unroll
+            for (int i = 0; i < NT * NT; ++i) {
+                // (a select against a lane-dependent value under a condition
+                // that always holds: the result is the constant, but not
+                // provably uniform)
+                Rr1[i] = a.n > 0 ? L.R1[i] : (T)lane;
+                Rr2[i] = a.n > 0 ? L.R2[i] : (T)lane;
+            }
+        }
+    }
     __device__ __forceinline__ bool has(int f) const
     {
         return KIND == K_GENERIC ? (flags & f) != 0 : (CF & f) != 0;
@@ -530,8 +553,13 @@ template <typename T, int NT, int NU, bool SPARSE, int KIND, int PERM> struct St
                     bool st;
                     if constexpr (P == 2) {
                         T p1[NT];
-                        restrict_reg<T, NT>(L.R1, r[0], p);
-                        restrict_reg<T, NT>(L.R2, r[1], p1);
+                        if constexpr (RTREG) {
+                            restrict_reg<T, NT>(Rr1, r[0], p);
+                            restrict_reg<T, NT>(Rr2, r[1], p1);
+                        } else {
+                            restrict_reg<T, NT>(L.R1, r[0], p);
+                            restrict_reg<T, NT>(L.R2, r[1], p1);
+                        }
 #pragma unroll
                         for (int i = 0; i < NT; ++i) p[i] = FP<T>::add(p[i], p1[i]);
                         st = true;
@@ -573,7 +601,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
 {
     constexpr bool WITH_C = KindProlongs<KIND>::value;
     using Lay = RowLayout<T, NT, WITH_C, KindLeaf<KIND>::value>;
-    using S = Streamer<T, NT, NU, SPARSE, KIND, PERM>;
+    using S = Streamer<T, NT, NU, SPARSE, KIND, PERM, KIND == K_DOWN && Lay::P == 2 && sizeof(T) == 8>;
     constexpr int P = S::P;
     constexpr int W = Lay::W;
     constexpr int G = Lay::G;
@@ -589,6 +617,7 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     if (a.active && !a.active[b]) return;
 
     S st{L, a, lane, a.flags};
+    st.transfer_regs();
     const long long n = a.n;
     st.nc = n >> 1;
     const long long nrows = (n + W - 1) / W;
@@ -1011,6 +1040,11 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
                     const __grid_constant__ StreamArgs<T> a, const __grid_constant__ StreamArgs<T> a1)
 {
     using Lay = RowLayoutD<T, NT>;
+#ifdef TMG_NO_RTREG
+    using S0 = Streamer<T, NT, NU, SPARSE, K_DOWN, PERM>;
+#else
+    using S0 = Streamer<T, NT, NU, SPARSE, K_DOWN, PERM, RowLayoutD<T, NT>::P == 2 && sizeof(T) == 8>;
+#endif
     using S = Streamer<T, NT, NU, SPARSE, K_DOWN, PERM>;
     constexpr int P = S::P, W = 32 * P;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1025,8 +1059,9 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
     if (a.active && !a.active[b]) return;
 
     const long long n = a.n, n1 = n >> 1, n2 = n >> 2;
-    S st{L, a, lane, a.flags};
+    S0 st{L, a, lane, a.flags};
     st.nc = n1;
+    st.transfer_regs();
     S s1{L1, a1, lane, a1.flags};
     s1.nc = n2;
     const long long row0 = chunk * a.rows_per_chunk;          // even; every row full (n % 128 == 0)

@@ -428,3 +428,31 @@ def test_scan_edges_guards_and_alignment(oracle_mod, p_t):
                 nrm = max(np.linalg.norm(exact), 1e-300)
                 assert np.linalg.norm(got[b] - exact) <= 1e-12 * nrm, (n, B, b, shift)
                 assert np.linalg.norm(got[b] - want) <= np.linalg.norm(want - exact) + 1e-12 * nrm
+
+
+@pytest.mark.parametrize("p_t", [0, 1, 2, 3])
+def test_scan_fp32_through_abi(oracle_mod, p_t):
+    """the fp32 instantiation of the scan solve (throughput variant: cp.async
+    pieces of 4 / 8 / 16 bytes, FMA arithmetic) against the extended-precision
+    solution, normwise 1e-4, aligned and unaligned right-hand sides"""
+    import torch
+    nt = p_t + 1
+    L = nat.load()
+    ops = tmg.assemble_local(tmg.BasisSpec(p_t), 1e-2)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for n, B in [(5000, 2), (257, 1), (128 * 9, 3)]:
+        rhs = np.random.default_rng(77 + n).standard_normal((B, n, nt)).astype(np.float32)
+        d = nat.level_desc(ops, n)
+        for shift in (0, 1):
+            fbuf = torch.zeros(B * n * nt + 4, dtype=torch.float32, device="cuda")
+            fv = fbuf[shift:shift + B * n * nt]
+            fv.copy_(torch.from_numpy(rhs.reshape(-1)))
+            u = torch.full((B * n * nt,), float("nan"), dtype=torch.float32, device="cuda")
+            nat.check(L.tmg_coarse_solve(nat.F32, ctypes.byref(d), ctypes.c_void_p(fv.data_ptr()),
+                                         ctypes.c_void_p(u.data_ptr()), B, 1, blas_tree.resolve(None), st),
+                      "tmg_coarse_solve fp32")
+            torch.cuda.synchronize()
+            got = u.cpu().numpy().reshape(B, n, nt).astype(np.float64)
+            for b in range(B):
+                exact = oracle_mod.forward_solve_extended(ops, rhs[b].astype(np.float64))
+                assert np.linalg.norm(got[b] - exact) <= 1e-4 * np.linalg.norm(exact), (n, B, b, shift)

@@ -166,6 +166,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// TMG_LONG_WARMUP: the row-wise warm-up everywhere (A/B)
+__device__ __forceinline__ constexpr bool warm_short()
+{
+#ifdef TMG_LONG_WARMUP
+    return false;
+#else
+    return true;
+#endif
+}
+
 template <int KIND> struct KindProlongs {
     static constexpr bool value = KIND != K_DOWN && KIND != K_DOWNNORM;
 };
@@ -940,7 +950,44 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         __syncwarp();
     };
 
-    if (row0 > 0) {
+    if (row0 > 0 && !FINEST && NU == 1 && warm_short()) {
+        // both levels from the zero guess with nu = 1: the pre-sweep needs no
+        // predecessor, so the carries depend on two level-(l+1) slabs and one
+        // level-l slab before the chunk (same functions, same bits as the rows)
+        using C = typename S::C;
+        const long long g0 = row0 * W;
+        const long long jc = (g0 >> 1) - 1;    // odd; jc - 1 is its even partner under one level-(l+2) slab
+        T fa[1][NT], fbb[1][NT], u2[NT], ua[1][NT], ub[1][NT];
+        load_slab_scalar<T, NT>(f1b + (jc - 1) * NT, fa[0]);
+        load_slab_scalar<T, NT>(f1b + jc * NT, fbb[0]);
+        load_slab_scalar<T, NT>(u2b + (jc >> 1) * NT, u2);
+        sweep_zero_j<T, NT, PERM, 1>(L1, ua, fa);
+        sweep_zero_j<T, NT, PERM, 1>(L1, ub, fbb);
+        prolong_reg<T, NT>(L1.R1, u2, ua[0]);
+        prolong_reg<T, NT>(L1.R2, u2, ub[0]);
+        const C ca[1] = {make_cpl<T, NT, SPARSE, true>(L1, ua[0])};
+        s1.carry[1] = make_cpl<T, NT, SPARSE, true>(L1, ub[0]);
+        T ubm[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) ubm[j] = ub[0][j];
+        const bool hp1[1] = {true};
+        sweep_j<T, NT, SPARSE, PERM, 1, true>(L1, ub, fbb, ca, hp1);   // level-(l+1) result at slab jc
+        T ff[1][NT], um[1][NT];
+        load_slab_scalar<T, NT>(fb + (g0 - 1) * NT, ff[0]);
+        sweep_zero_j<T, NT, PERM, 1>(L, um, ff);
+        prolong_reg<T, NT>(L.R2, ub[0], um[0]);
+        st.carry[1] = make_cpl<T, NT, SPARSE, true>(L, um[0]);
+        if constexpr (S::TRACK) {
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    s1.rec[NT + j] = (unsigned)__double2hiint((double)ubm[j]);
+                    st.rec[NT + j] = (unsigned)__double2hiint((double)um[0][j]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (row0 > 0) {
         // warm-up: the coarse row before the chunk, then the fine row before it
         const long long cw = (row0 >> 1) - 1;
         T f1[P][NT], u2[NT];
@@ -1150,7 +1197,51 @@ __global__ void __launch_bounds__(CtaShape<T, NT>::WARPS * 32, CtaShape<T, NT>::
         __syncwarp();
     };
 
-    if (row0 > 0) {
+    if (row0 > 0 && NU == 1 && warm_short()) {
+        // nu1 = 1 from the zero guess: the first sweep needs no predecessor, so
+        // the chunk depends on only THREE level-l slabs before it -- their
+        // zero-guess sweeps, the residuals of the last two, their restriction
+        // and that level-(l+1) slab's zero-guess sweep give both levels'
+        // carries (every lane computes the same scalars; same functions, same
+        // bits as the row path) instead of three level-l rows and one
+        // level-(l+1) row: the small levels' kernels are mostly warm-up.
+        using C = typename S::C;
+        const long long g0 = row0 * W;
+        T f3[3][NT], u3[3][NT];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) load_slab_scalar<T, NT>(fb + (g0 - 3 + i) * NT, f3[i]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            T uu[1][NT], ff[1][NT];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) ff[0][j] = f3[i][j];
+            sweep_zero_j<T, NT, PERM, 1>(L, uu, ff);
+#pragma unroll
+            for (int j = 0; j < NT; ++j) u3[i][j] = uu[0][j];
+        }
+        const C c0 = make_cpl<T, NT, SPARSE, true>(L, u3[0]);
+        const C c1 = make_cpl<T, NT, SPARSE, true>(L, u3[1]);
+        st.carry[NU] = make_cpl<T, NT, SPARSE, true>(L, u3[2]);
+        T r0[NT], r1[NT], pc[1][NT], p1[NT], uc1[1][NT];
+        residual<T, NT, SPARSE, true>(L, u3[1], f3[1], c0, true, r0);
+        residual<T, NT, SPARSE, true>(L, u3[2], f3[2], c1, true, r1);
+        restrict_reg<T, NT>(L.R1, r0, pc[0]);
+        restrict_reg<T, NT>(L.R2, r1, p1);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) pc[0][j] = FP<T>::add(pc[0][j], p1[j]);
+        sweep_zero_j<T, NT, PERM, 1>(L1, uc1, pc);
+        s1.carry[NU] = make_cpl<T, NT, SPARSE, true>(L1, uc1[0]);
+        if constexpr (S::TRACK) {
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    st.rec[NU * NT + j] = (unsigned)__double2hiint((double)u3[2][j]);
+                    s1.rec[NU * NT + j] = (unsigned)__double2hiint((double)uc1[0][j]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (row0 > 0) {
         // warm-up: level-l rows row0-3 (carries only), row0-2 and row0-1 (the
         // level-(l+1) row before the chunk), then that row (carries only)
         for (long long r = max(0LL, row0 - 3); r < row0; ++r) {

@@ -413,13 +413,25 @@ template <typename T, int NT, bool SPARSE, bool SMEM> struct Engine {
             chunk(n, a, e);
             if (a < e) {
                 const LevelC<T, NT> &L = Lv(l);
-                const int hs = max(0, a - (nu + 1)) & ~1;
+                int hs = max(0, a - (nu + 1)) & ~1;
                 const T *f = F(l), *u = U(l);
                 T *pre = Pre(l), *fc = F(l + 1);
                 C cin[TAIL_MAXNU], cres;  // predecessor data per sweep / for the residual
 #pragma unroll
                 for (int k = 0; k < TAIL_MAXNU; ++k) cpl_zero(cin[k]);
                 cpl_zero(cres);
+                if (zg && nu == 1 && a > 0) {
+                    // one sweep from the zero guess has no predecessor: all the
+                    // chunk needs from its left is the swept slab a-1 (for the
+                    // residual of slab a) -- one zero-guess sweep instead of a
+                    // re-derived pair with its residuals
+                    T fh[NT], xh[NT];
+                    load(f + (a - 1) * NT, fh);
+                    zero_slab<T, NT>(xh);
+                    sweep_zero1(L, xh, fh);
+                    cres = make_cpl<T, NT, SPARSE>(L, xh);
+                    hs = a;
+                }
                 for (int j = hs; j < e; j += 2) {
                     T x0[NT], x1[NT], f0[NT], f1[NT];
                     load(f + j * NT, f0);
@@ -491,12 +503,22 @@ template <typename T, int NT, bool SPARSE, bool SMEM> struct Engine {
             chunk(n, a, e);
             if (a < e) {
                 const LevelC<T, NT> &L = Lv(l);
-                const int hs = max(0, a - nu) & ~1;
+                int hs = max(0, a - nu) & ~1;
                 const T *f = F(l), *pre = Pre(l), *uc = U(l + 1);
                 T *u = U(l);
                 C cin[TAIL_MAXNU];
 #pragma unroll
                 for (int k = 0; k < TAIL_MAXNU; ++k) cpl_zero(cin[k]);
+                if (nu == 1 && a > 0) {
+                    // one post-sweep: the chunk needs only the prolongated
+                    // (unswept) slab a-1 from its left -- no re-derived pair
+                    T xh[NT], c[NT];
+                    load(pre + (a - 1) * NT, xh);
+                    load(uc + ((a - 1) >> 1) * NT, c);
+                    prolong_part<T, NT>(L, c, true, xh);   // a is even: slab a-1 is odd
+                    cin[0] = make_cpl<T, NT, SPARSE>(L, xh);
+                    hs = a;
+                }
                 for (int j = hs; j < e; j += 2) {
                     T x0[NT], x1[NT], f0[NT], f1[NT], c[NT];
                     load(pre + j * NT, x0);

@@ -374,7 +374,10 @@ int chunk_rows(long long n, long long batch, int leaf_rows, int w, int stage)
         rmax = x ? std::max(rmin, atoi(x)) : 64;  // 32-96 measured ~1 % better than 128 on config 3
     }
     const long long target_warps = (long long)sm_count() * 16 * waves;
-    long long r = (rows * batch) / std::max(1LL, target_warps);
+    // rounded UP: rounded down, 16384 rows over 2368 warps gave 6-row chunks,
+    // 2731 of them -- a second, nearly empty wave (config 2's finest pass:
+    // 36 -> 27 us with 8-row chunks)
+    long long r = (rows * batch + target_warps - 1) / std::max(1LL, target_warps);
     r = std::max((long long)rmin, std::min((long long)rmax, r));
     // a multiple of the ring stage (stage_slabs) and of the norm leaf
     const int g = stage / w;

@@ -85,3 +85,20 @@ def test_rhs_entry_points_validate_without_gpu(lib):
     assert rc == nat.E_ARG and b"n_t" in lib.tmg_rhs_last_error()
     rc = lib.tmg_rhs_sines(None, None, None, p, 8, -1.0, 0.1, 0.0, p, p, p, 2, 2, None, 4, 1, None)
     assert rc == nat.E_ARG
+
+
+def test_stream_split_and_phase_buckets(monkeypatch):
+    """host logic of the streamed host pipeline and of SolveStats.times:
+    sub-batches per batch (halves from 32 problems up, env override that must
+    divide B) and the kernel-name -> phase mapping of the traced solve"""
+    from paper_1409_5254_b200 import solver
+    monkeypatch.delenv("TMG_STREAM_SPLIT", raising=False)
+    assert solver._stream_split(64) == 2 and solver._stream_split(32) == 2
+    assert solver._stream_split(16) == 1 and solver._stream_split(33) == 1 and solver._stream_split(1) == 1
+    monkeypatch.setenv("TMG_STREAM_SPLIT", "4")
+    assert solver._stream_split(64) == 4 and solver._stream_split(6) == 1
+    assert solver._phase_bucket("tail_kernel") == "coarse"
+    assert solver._phase_bucket("stream_kernel_v (level-1 up + finest up + next finest down)") == "smoothing"
+    assert solver._phase_bucket("stream_kernel<nt=2,nu=1,kind=1> n=2048 flags=135") == "smoothing"
+    assert solver._phase_bucket("finalize") == "residual" and solver._phase_bucket("set_active") == "residual"
+    assert set(solver._times(1.5)) == {"smoothing", "transfer", "coarse", "residual"}
